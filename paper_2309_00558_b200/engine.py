@@ -1,0 +1,177 @@
+"""Public entry points: ``run`` / ``compare_policies`` / ``run_batch``.
+
+Drop-in for sim_engine.py:601-612.  A call compiles each (scenario, policy)
+on the host (``compiler.py``), executes the whole batch in the sm_100a kernel
+through the C ABI (``backend.py``), and decodes the fixed-size device records
+into the reference's ``MetricsReport`` rows, in the reference's append order
+(sim_engine.py:555-589), so ``to_csv()`` / ``summary()`` are byte-identical.
+
+There is no CPU fallback: without the CUDA library or a GPU every call raises
+``BackendUnavailableError``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import compiler as cc
+from .errors import CapacityError, InvariantError, ValidationError
+from .metrics import FunctionWindowRow, GlobalWindowRow, GpuWindowRow, MetricsReport
+from .scenario import POLICIES
+
+_MAX_CAP_RETRIES = 8
+
+
+@dataclass
+class RunResult:
+    """Everything one device run reports."""
+
+    report: MetricsReport
+    # final packer state: node -> {pod_id: (x, y, w, h) as exact Fractions}
+    placements: dict = field(default_factory=dict)
+    token_grants: int = 0
+    scale_decisions: int = 0
+    placement_attempts: int = 0
+
+    @property
+    def decisions(self) -> int:
+        return self.token_grants + self.scale_decisions + self.placement_attempts
+
+
+def run_error(image: cc.RunImage, status) -> Exception | None:
+    """Map a device status record to the exception the reference would raise."""
+    code = int(status["code"])
+    if code == cc.GS_OK:
+        return None
+    if code == cc.GS_ERR_VALIDATION:
+        f, k = int(status["arg0"]), int(status["arg1"])
+        sm_eff = float(image.points[k + int(image.funcs[f]["point_off"])]["sm_eff"])
+        # sim_engine.py:346-349
+        return ValidationError(f"{image.fids[f]}: zero serving rate at ({sm_eff:g}, 1.0)")
+    if code == cc.GS_ERR_CAPACITY:
+        return CapacityError(f"device capacity exceeded (detail {int(status['detail'])})")
+    if code == cc.GS_ERR_INVARIANT:
+        return InvariantError(f"device reported an invariant breach (detail "
+                              f"{int(status['detail'])}, {int(status['arg0'])}, "
+                              f"{int(status['arg1'])})")
+    return InvariantError(f"device returned code {code}")
+
+
+def decode_run(batch: cc.Batch, r: int, out: dict) -> RunResult:
+    """Rebuild the reference's report rows for run ``r`` from device records."""
+    im = batch.images[r]
+    s = batch.runs[r]
+    W, F, G = int(s["windows"]), int(s["n_funcs"]), int(s["n_nodes"])
+    rep = MetricsReport(policy=im.policy)
+    fn = out["fn_rows"][int(s["fn_row_off"]): int(s["fn_row_off"]) + W * F]
+    gp = out["gpu_rows"][int(s["gpu_row_off"]): int(s["gpu_row_off"]) + W * G]
+    gl = out["glob_rows"][int(s["glob_row_off"]): int(s["glob_row_off"]) + W]
+    fids = im.fids
+    fn_l = fn.tolist()
+    gp_l = gp.tolist()
+    gl_l = gl.tolist()
+    for w in range(W):
+        for f in range(F):
+            a, c, v, d, q = fn_l[w * F + f]
+            rep.function_rows.append(FunctionWindowRow(w, fids[f], a, c, v, d, q))
+        for g in range(G):
+            u, o, m, present, _ = gp_l[w * G + g]
+            if present:
+                rep.gpu_rows.append(GpuWindowRow(w, g, u, o, m))
+        n_use, fails, frag = gl_l[w]
+        rep.global_rows.append(GlobalWindowRow(w, n_use, fails, frag))
+    st = out["status"][r]
+    res = RunResult(rep, token_grants=int(st["token_grants"]),
+                    scale_decisions=int(st["scale_decisions"]),
+                    placement_attempts=int(st["placement_attempts"]))
+    pl = out["placements"][int(s["place_off"]): int(s["place_off"]) + int(st["n_placements"])]
+    nodes: dict = {g: {} for g in range(G)}
+    for node, func, counter, x, y, w_, h, _ in pl.tolist():
+        pod_id = f"{fids[func]}-{counter:04d}"
+        nodes[node][pod_id] = (Fraction(x, im.scale_x), Fraction(y, im.scale_y),
+                               Fraction(w_, im.scale_x), Fraction(h, im.scale_y))
+    res.placements = nodes
+    return res
+
+
+def _normalise(scenarios, policies):
+    scenarios = list(scenarios)
+    if isinstance(policies, str):
+        policies = [policies] * len(scenarios)
+    policies = list(policies)
+    if len(policies) != len(scenarios):
+        raise ValidationError("need one policy per scenario")
+    return scenarios, policies
+
+
+def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
+             rows: bool = True) -> list:
+    """Run a batch of (scenario, policy) pairs on the GPU.
+
+    Returns one ``RunResult`` per input (or the exception, when
+    ``errors="return"``).  Runs that outgrow a static device capacity are
+    re-executed on the device with doubled capacities; nothing is truncated.
+    """
+    from . import backend
+    scenarios, policies = _normalise(scenarios, policies)
+    results: list = [None] * len(scenarios)
+    images: list = [None] * len(scenarios)
+    for i, (sc, pol) in enumerate(zip(scenarios, policies)):
+        try:
+            images[i] = cc.compile_run(sc, pol)
+        except ValidationError as exc:
+            if errors == "raise":
+                raise
+            results[i] = exc
+    pending = [i for i in range(len(scenarios)) if images[i] is not None]
+    for _attempt in range(_MAX_CAP_RETRIES):
+        if not pending:
+            break
+        batch = cc.Batch([images[i] for i in pending])
+        out = backend.run_batch(batch, device=device, rows=True)
+        retry = []
+        for j, i in enumerate(pending):
+            st = out["status"][j]
+            if int(st["code"]) == cc.GS_ERR_CAPACITY:
+                caps = cc.Caps(int(batch.runs[j]["cap_pods"]), int(batch.runs[j]["cap_rects"]),
+                               int(batch.runs[j]["cap_returned"])).grown(int(st["detail"]))
+                images[i] = cc.compile_run(scenarios[i], policies[i], caps)
+                retry.append(i)
+                continue
+            err = run_error(batch.images[j], st)
+            if err is not None:
+                if errors == "raise":
+                    raise err
+                results[i] = err
+            else:
+                results[i] = decode_run(batch, j, out)
+        pending = retry
+    for i in pending:
+        err = CapacityError("run still exceeds device capacities after "
+                            f"{_MAX_CAP_RETRIES} enlargements")
+        if errors == "raise":
+            raise err
+        results[i] = err
+    return results
+
+
+def run_batch(scenarios, policies="fast", *, device: int = 0, errors: str = "raise") -> list:
+    """Batch form of ``run``: one ``MetricsReport`` (or exception) per input."""
+    return [r.report if isinstance(r, RunResult) else r
+            for r in simulate(scenarios, policies, device=device, errors=errors)]
+
+
+def run(scenario, policy: str = "fast") -> MetricsReport:
+    """Simulate one scenario under one policy (sim_engine.py:601-603)."""
+    return simulate([scenario], [policy])[0].report
+
+
+def compare_policies(scenario, policies=POLICIES) -> dict:
+    """Each policy on the same scenario, fresh state (sim_engine.py:606-612)."""
+    for p in policies:
+        if p not in POLICIES:
+            raise ValidationError(f"unknown policy {p!r}")
+    res = simulate([scenario] * len(policies), list(policies))
+    return {p: r.report for p, r in zip(policies, res)}

@@ -1,0 +1,224 @@
+"""Generate the golden fixtures that pin the oracle (and the GPU path).
+
+Runs the REAL reference package (imported read-only from
+/root/reference/pkg/src) on
+
+  * the three bundled scenarios (pkg/scenarios/*.json) x both policies,
+  * the constructed scenarios of the reference's own engine tests
+    (pkg/tests/test_sim_engine.py make_scenario variants, :22-195),
+  * a seeded random sweep that exercises every engine branch: epochs,
+    scale-up/down with in-flight requests, retry, memory-gated placement,
+    restructure, max_queue drops, fractional quotas / SM partitions, CSV
+    profiles with zero-throughput points, timeshare validation errors,
+
+and records for each (scenario, policy) the metrics CSV (or the exception
+text), the summary, and the final packer placements.  Usage (in the build
+container only -- the reference does not exist on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Output: tests/golden/golden_runs.json.gz (committed).
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import random
+import sys
+import tempfile
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(HERE, "golden_runs.json.gz")
+
+FID_POOL = ["resnet_v1", "rnnt_asr", "bert_qa", "bert", "bert2", "vit", "A", "a_b",
+            "gpt.small", "z9", "Resnet", "yolo", "m"]
+SM_POOL = [6, 12, 24, 50, 60, 80, 100, 12.5, 33, 40, 75]
+Q_POOL = [0.2, 0.4, 0.6, 0.8, 0.1, 0.25, 0.5, 0.75, 0.3, 0.35]
+
+
+def _synth(rng, with_100):
+    sms = sorted(set(rng.sample(SM_POOL, rng.randint(1, 5)) + ([100] if with_100 else [])))
+    qs = sorted(set(rng.sample(Q_POOL, rng.randint(0, 4)) + [1.0]))
+    return {
+        "t_max": round(rng.uniform(4, 120), rng.choice([0, 1, 3])),
+        "sm_knee": rng.choice([6.0, 12.0, 24.0, 50.0, 100.0, 37.5]),
+        "grid_sm": sms, "grid_quota": qs,
+        "slo_ms": rng.choice([50.0, 100.0, 250.0, 500.0, 1000.0, 2000.0]),
+        "mem": {"mem_noshare_mb": rng.choice([1200.0, 1600.0, 2500.0, 700.5]),
+                "mem_runtime_mb": rng.choice([900.0, 1100.0, 400.0, 333.3]),
+                "mem_server_mb": rng.choice([600.0, 800.0, 1500.0, 250.25])},
+    }, sms, qs
+
+
+def _csv_profile(rng, fid, with_100):
+    sms = sorted(set(rng.sample(SM_POOL, rng.randint(1, 4)) + ([100] if with_100 else [])))
+    qs = sorted(set(rng.sample(Q_POOL, rng.randint(0, 3)) + [1.0]))
+    lines = ["function_id,sm_partition,quota,throughput_rps,p99_ms,slo_ms,"
+             "mem_noshare_mb,mem_runtime_mb,mem_server_mb"]
+    slo = rng.choice([100.0, 400.0, 1000.0])
+    for sm in sms:
+        for q in qs:
+            t = round(rng.uniform(0.5, 60.0) * q, 3)
+            if rng.random() < 0.06:
+                t = 0.0
+            lines.append(f"{fid},{sm},{q},{t},{round(1000.0 / max(t, 1e-3), 3)},{slo},"
+                         f"1300,950,650")
+    return "\n".join(lines) + "\n", sms, qs
+
+
+def _trace(rng, windows):
+    kind = rng.choice(["constant", "constant", "step", "sinusoid", "explicit", "explicit"])
+    pois = rng.random() < 0.4
+    if kind == "constant":
+        t = {"kind": "constant", "rps": round(rng.uniform(0, 70), rng.choice([0, 2]))}
+    elif kind == "step":
+        t = {"kind": "step", "base_rps": round(rng.uniform(0, 40), 1),
+             "step_rps": round(rng.uniform(0, 90), 1), "step_window": rng.randint(0, windows)}
+    elif kind == "sinusoid":
+        t = {"kind": "sinusoid", "base_rps": round(rng.uniform(0, 50), 1),
+             "amplitude_rps": round(rng.uniform(0, 40), 1),
+             "period_windows": rng.randint(1, max(1, windows))}
+    else:
+        n = rng.randint(0, windows + 3)
+        t = {"kind": "explicit", "counts": [
+            rng.choice([0, 0, rng.randint(0, 15), rng.randint(10, 120)]) for _ in range(n)]}
+        pois = False
+    if pois:
+        t["poisson"] = True
+        if rng.random() < 0.7:
+            t["seed"] = rng.randint(0, 10 ** 6)
+    return t
+
+
+def random_case(rng, idx):
+    windows = rng.randint(2, 22)
+    files = {}
+    fns = []
+    fids = rng.sample(FID_POOL, rng.randint(1, 5))
+    with_100 = rng.random() < 0.8
+    for fid in fids:
+        if rng.random() < 0.18:
+            text, sms, qs = _csv_profile(rng, fid, with_100)
+            files[f"{fid}.csv"] = text
+            prof = {"csv": f"{fid}.csv"}
+        else:
+            synth, sms, qs = _synth(rng, with_100)
+            prof = {"synth": synth}
+        inits = []
+        for _ in range(rng.choice([0, 1, 1, 2, 3, 5])):
+            p = {"sm": rng.choice(sms), "quota": rng.choice(qs)}
+            if rng.random() < 0.2:
+                p["quota_request"] = round(p["quota"] * rng.choice([0.5, 0.9, 1.0]), 3)
+            inits.append(p)
+        fn = {"function_id": fid, "profile": prof, "trace": _trace(rng, windows),
+              "initial_pods": inits}
+        if rng.random() < 0.15:
+            fn["max_queue"] = rng.randint(0, 25)
+        fns.append(fn)
+    sc = {
+        "fleet_size": rng.choice([1, 1, 2, 2, 3, 4]),
+        "windows": windows,
+        "epoch_windows": rng.randint(1, 6),
+        "quantum": rng.choice([0.02, 0.02, 0.05, 0.1, 0.25, 0.5, 1.0, 0.04, 0.125, 0.01]),
+        "cold_start_windows": rng.randint(0, 3),
+        "seed": rng.randint(0, 1000),
+        "functions": fns,
+    }
+    if rng.random() < 0.3:
+        sc["window_ms"] = rng.choice([500.0, 250.0, 2000.0, 100.0, 333.0, 1500.0])
+    if rng.random() < 0.3:
+        sc["model_sharing"] = False
+    if rng.random() < 0.35:
+        sc["gpu_capacity_mb"] = rng.choice([3000.0, 4000.0, 8000.0, 81920.0, 5500.5])
+    if rng.random() < 0.35:
+        sc["restructure_threshold"] = rng.choice([0, 1, 2, 3, 4, 8])
+    return {"name": f"random-{idx:04d}", "scenario": sc, "files": files}
+
+
+def engine_test_cases():
+    """The constructed scenarios of pkg/tests/test_sim_engine.py:22-195 as dicts."""
+    def mk(name, t_max=10.0, knee=24.0, rps=10.0, windows=8, fleet_size=1, epoch_windows=5,
+           cold=2, initial=((24, 1.0),), slo=250.0, grid_sm=(6, 12, 24, 50, 100),
+           grid_quota=(0.2, 0.4, 0.6, 0.8, 1.0), max_queue=None):
+        fn = {"function_id": "fn",
+              "profile": {"synth": {"t_max": t_max, "sm_knee": knee, "grid_sm": list(grid_sm),
+                                    "grid_quota": list(grid_quota), "slo_ms": slo}},
+              "trace": {"kind": "constant", "rps": rps},
+              "initial_pods": [{"sm": s, "quota": q} for s, q in initial]}
+        if max_queue is not None:
+            fn["max_queue"] = max_queue
+        return {"name": name, "files": {}, "scenario": {
+            "fleet_size": fleet_size, "windows": windows, "epoch_windows": epoch_windows,
+            "cold_start_windows": cold, "functions": [fn]}}
+    return [
+        mk("engine-steady"),
+        mk("engine-zero-arrivals", rps=0.0, windows=6, epoch_windows=2),
+        mk("engine-overload", rps=100.0, epoch_windows=2, cold=0, grid_sm=(24,),
+           grid_quota=(1.0,), slo=10000.0),
+        mk("engine-cold-start", rps=5.0, windows=6, epoch_windows=1, cold=2, initial=(),
+           slo=100.0),
+        mk("engine-empty", rps=0.0, windows=4, epoch_windows=2, initial=()),
+        mk("engine-full-gpu", rps=5.0, windows=4, initial=((100, 1.0),)),
+        mk("engine-dropped", rps=50.0, windows=3, grid_sm=(24,), grid_quota=(1.0,),
+           slo=10000.0, max_queue=5, epoch_windows=10),
+    ]
+
+
+def bundled_cases():
+    out = []
+    sdir = "/root/reference/pkg/scenarios"
+    for name in sorted(os.listdir(sdir)):
+        with open(os.path.join(sdir, name)) as fh:
+            out.append({"name": "bundled-" + name[:-5], "files": {}, "scenario": json.load(fh)})
+    # the survey's C1: consolidation at 1 node, 60 windows
+    with open(os.path.join(sdir, "consolidation.json")) as fh:
+        c1 = json.load(fh)
+    c1.update({"fleet_size": 1, "windows": 60, "epoch_windows": 5, "cold_start_windows": 2})
+    out.append({"name": "survey-C1", "files": {}, "scenario": c1})
+    return out
+
+
+def run_reference(case, policy):
+    sys.path.insert(0, REF)
+    import gshare_sim as ref
+    from gshare_sim.sim_engine import _Engine
+    with tempfile.TemporaryDirectory() as tmp:
+        for fname, text in case["files"].items():
+            with open(os.path.join(tmp, fname), "w") as fh:
+                fh.write(text)
+        try:
+            sc = ref.Scenario.from_dict(json.loads(json.dumps(case["scenario"])), base_dir=tmp)
+            eng = _Engine(sc, policy)
+            report = eng.run()
+        except ref.GShareError as exc:
+            return {"error": type(exc).__name__, "message": str(exc)}
+    placements = []
+    for node in eng.nodes:
+        for pid, p in sorted(node.placements.items()):
+            r = p.rect
+            placements.append([node.gpu_id, pid] + [f"{v.numerator}/{v.denominator}"
+                                                    for v in (r.x, r.y, r.w, r.h)])
+    return {"csv": report.to_csv(), "summary": report.summary(), "placements": placements}
+
+
+def main(n_random: int = 360, seed: int = 20261017):
+    rng = random.Random(seed)
+    cases = bundled_cases() + engine_test_cases() + [random_case(rng, i) for i in range(n_random)]
+    records = []
+    for case in cases:
+        for policy in ("fast", "timeshare"):
+            rec = dict(case)
+            rec["policy"] = policy
+            rec["expect"] = run_reference(case, policy)
+            records.append(rec)
+    with gzip.open(OUT, "wt", encoding="utf-8") as fh:
+        json.dump({"generator": "tests/golden/make_golden.py", "seed": seed,
+                   "reference": "pkg/src/gshare_sim 0.1.0", "records": records}, fh)
+    n_err = sum(1 for r in records if "error" in r["expect"])
+    print(f"wrote {len(records)} records ({n_err} reference errors) to {OUT}")
+
+
+if __name__ == "__main__":
+    main()

@@ -158,6 +158,8 @@ typedef struct gs_status {
   int64_t token_grants;          /* dispatch() outputs, token_backend.py:186     */
   int64_t scale_decisions;       /* len(scale_up)+len(scale_down)                */
   int64_t placement_attempts;    /* best_match calls, sim_engine.py:397          */
+  int64_t pod_steps;             /* sum over quantum steps of registered pods    */
+  int64_t rect_scans;            /* free rects examined by best_match            */
 } gs_status_t;
 
 /* Fixed-size per-run record all-gathered across GPUs (metrics.py:94-131). */

@@ -77,7 +77,7 @@ typedef struct {
   Node* nodes;
   int* retry; int nretry, cretry;
   int win_failures;
-  long long grants, decisions, attempts;
+  long long grants, decisions, attempts, pod_steps, rect_scans;
   int err_code, err_fn, err_pt;
 } Eng;
 
@@ -210,6 +210,7 @@ static int best_match(const Eng* e, const Pod* p, int* out_node, Rect* out_rect)
   for (int g = 0; g < e->G; g++) {
     const Node* n = &e->nodes[g];
     if (!admit(e, n, p->fn)) continue;
+    ((Eng*)e)->rect_scans += n->nfr;
     for (int i = 0; i < n->nfr; i++) {
       Rect r = n->fr[i];
       if (p->rw <= r.w && p->rh <= r.h) {
@@ -655,6 +656,11 @@ static int run_one(const gs_batch_t* in, int run, const gs_out_t* out) {
       for (int i = 0; i < n; i++) fn->fut[fn->fhead + fn->fn_ + i] = start + ((double)i * sc->window_s) / (double)n;
       fn->fn_ += n;
     }
+    {
+      long long nreg = 0;
+      for (int i = 0; i < e->npods; i++) nreg += e->pods[i].alive && e->pods[i].registered;
+      e->pod_steps += nreg * sc->steps;
+    }
     run_window_steps(e, w);
     /* _close_window */
     for (int f = 0; f < e->F; f++) {
@@ -728,6 +734,8 @@ done:
   st->token_grants = e->grants;
   st->scale_decisions = e->decisions;
   st->placement_attempts = e->attempts;
+  st->pod_steps = e->pod_steps;
+  st->rect_scans = e->rect_scans;
   if (out->summary) out->summary[run] = sum;
   free_engine(e);
   return st->code;

@@ -1,1 +1,126 @@
-"""placeholder"""
+"""ctypes binding of the CUDA library (libgshare_b200.so, built in-tree).
+
+This is the only execution path of the package.  If the library is missing or
+no CUDA device is visible every entry point raises BackendUnavailableError --
+there is deliberately no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .abi import make_batch_struct, make_out_struct
+from .errors import BackendUnavailableError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libgshare_b200.so")
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise BackendUnavailableError(
+                    f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+            L = C.CDLL(LIB_PATH)
+            vp, i, sz, cp = C.c_void_p, C.c_int, C.c_size_t, C.c_char_p
+            L.gs_abi_version.restype = i
+            L.gs_run_batch.argtypes = [vp, vp, i, vp, cp, sz]
+            L.gs_run_batch.restype = i
+            L.gs_session_create.argtypes = [vp, i, C.POINTER(vp), cp, sz]
+            L.gs_session_create.restype = i
+            L.gs_session_run.argtypes = [vp, vp, cp, sz]
+            L.gs_session_run.restype = i
+            L.gs_session_download.argtypes = [vp, vp, vp, cp, sz]
+            L.gs_session_download.restype = i
+            L.gs_session_device_out.argtypes = [vp, vp]
+            L.gs_session_device_out.restype = i
+            L.gs_session_last_launches.argtypes = [vp]
+            L.gs_session_last_launches.restype = i
+            L.gs_session_last_kernel_ms.argtypes = [vp]
+            L.gs_session_last_kernel_ms.restype = C.c_double
+            L.gs_session_destroy.argtypes = [vp]
+            L.gs_session_destroy.restype = None
+            L.gs_set_launch.argtypes = [i, i]
+            L.gs_set_launch.restype = i
+            if L.gs_abi_version() != 1:
+                raise BackendUnavailableError("libgshare_b200.so ABI version mismatch")
+            _lib = L
+        return _lib
+
+
+def _check(rc: int, err, what: str):
+    from .compiler import GS_ERR_CUDA, GS_ERR_ARG
+    if rc in (GS_ERR_CUDA, GS_ERR_ARG):
+        raise BackendUnavailableError(f"{what}: {err.value.decode(errors='replace')}")
+
+
+def run_batch(batch, device: int = 0, rows: bool = True, stream=None) -> dict:
+    """One-shot: host arrays -> device -> kernel -> host output arrays."""
+    L = lib()
+    out = batch.alloc_outputs(rows=rows)
+    b = make_batch_struct(batch)
+    o = make_out_struct(out)
+    err = C.create_string_buffer(512)
+    rc = L.gs_run_batch(C.byref(b), C.byref(o), int(device), stream, err, len(err))
+    _check(rc, err, "gs_run_batch")
+    return out
+
+
+class Session:
+    """Inputs, workspace and outputs resident in HBM (bench / repeated runs)."""
+
+    def __init__(self, batch, device: int = 0):
+        self._lib = lib()
+        self.batch = batch
+        self._b = make_batch_struct(batch)
+        self.handle = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = self._lib.gs_session_create(C.byref(self._b), int(device), C.byref(self.handle),
+                                         err, len(err))
+        _check(rc, err, "gs_session_create")
+        if rc != 0:
+            raise BackendUnavailableError(f"gs_session_create failed ({rc})")
+
+    def run(self, stream=None) -> float:
+        err = C.create_string_buffer(512)
+        rc = self._lib.gs_session_run(self.handle, stream, err, len(err))
+        _check(rc, err, "gs_session_run")
+        return self._lib.gs_session_last_kernel_ms(self.handle)
+
+    def launches(self) -> int:
+        return self._lib.gs_session_last_launches(self.handle)
+
+    def download(self, rows: bool = True, stream=None) -> dict:
+        out = self.batch.alloc_outputs(rows=rows)
+        o = make_out_struct(out)
+        err = C.create_string_buffer(512)
+        rc = self._lib.gs_session_download(self.handle, C.byref(o), stream, err, len(err))
+        _check(rc, err, "gs_session_download")
+        return out
+
+    def device_out(self):
+        from .abi import GsOut
+        o = GsOut()
+        self._lib.gs_session_device_out(self.handle, C.byref(o))
+        return o
+
+    def close(self):
+        if self.handle:
+            self._lib.gs_session_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def set_launch(warps_per_block: int = 0, blocks_per_sm: int = -1):
+    lib().gs_set_launch(int(warps_per_block), int(blocks_per_sm))

@@ -26,7 +26,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 from fractions import Fraction
-from functools import reduce
+from functools import lru_cache, reduce
 
 import numpy as np
 
@@ -84,7 +84,8 @@ PLACEMENT_DT = np.dtype([("node", "<i4"), ("func", "<i4"), ("counter", "<i4"),
 STATUS_DT = np.dtype([("code", "<i4"), ("detail", "<i4"), ("arg0", "<i4"), ("arg1", "<i4"),
                       ("n_placements", "<i4"), ("pad", "<i4"),
                       ("token_grants", "<i8"), ("scale_decisions", "<i8"),
-                      ("placement_attempts", "<i8")], align=True)
+                      ("placement_attempts", "<i8"), ("pod_steps", "<i8"),
+                      ("rect_scans", "<i8")], align=True)
 SUMMARY_DT = np.dtype([("windows", "<i4"), ("gpus_used_peak", "<i4"),
                        ("placement_failures", "<i4"), ("n_gpu_rows", "<i4"),
                        ("arrivals", "<i8"), ("completions", "<i8"),
@@ -114,12 +115,13 @@ class Caps:
 
     def grown(self, detail: int) -> "Caps":
         if detail == GS_CAP_PODS:
-            return Caps(self.pods * 2, self.rects, self.returned)
+            return Caps(self.pods * 4, self.rects, self.returned)
         if detail == GS_CAP_RECTS:
-            return Caps(self.pods, min(self.rects * 2, _MAX_RECTS_CAP), self.returned)
-        return Caps(self.pods, self.rects, self.returned * 2)
+            return Caps(self.pods, min(self.rects * 4, _MAX_RECTS_CAP), self.returned)
+        return Caps(self.pods, self.rects, self.returned * 4)
 
 
+@lru_cache(maxsize=65536)
 def as_frac(value) -> Fraction:
     """The reference's coordinate snapping (packer.py:39-53)."""
     if isinstance(value, Fraction):
@@ -187,7 +189,63 @@ def _default_caps(scenario, fns) -> Caps:
         peak = max(counts, default=0) / window_s
         pods += len(fn.initial_pods) + int(math.ceil(1.5 * peak / t_eff)) + 4
     pods = min(max(32, -(-pods // 32) * 32), 1 << 20)
-    return Caps(pods=pods, rects=32, returned=8)
+    return Caps(pods=pods, rects=64, returned=32)
+
+
+@dataclass(frozen=True)
+class _LoweredProfile:
+    keys: list            # [(sm, quota)] sorted
+    index: dict
+    rows: np.ndarray      # POINT_DT without rect_w/rect_h
+    w_num: tuple
+    w_den: tuple
+    h_num: tuple
+    h_den: tuple
+    p_eff: int
+    sm_integral: bool
+
+
+_LOWER_CACHE: dict = {}
+
+
+def _lower_profile(profile, timeshare: bool) -> _LoweredProfile:
+    """Policy-specific dense point table of one profile (cached by content:
+    sweeps reuse a handful of profiles across thousands of scenarios)."""
+    pts = sorted(profile.entries)
+    ckey = (timeshare, tuple((p.sm_partition, p.quota, profile.entries[p].throughput_rps)
+                             for p in pts))
+    hit = _LOWER_CACHE.get(ckey)
+    if hit is not None:
+        return hit
+    tab = {(p.sm_partition, p.quota): e.throughput_rps for p, e in profile.entries.items()}
+    keys = [(p.sm_partition, p.quota) for p in pts]
+    rows = np.zeros(len(pts), POINT_DT)
+    w_num, w_den, h_num, h_den = [], [], [], []
+    best = None
+    integral = True
+    for i, p in enumerate(pts):
+        thr = profile.entries[p].throughput_rps
+        area = p.resource_area
+        rpr = thr / area
+        sm_eff = 100.0 if timeshare else p.sm_partition
+        rate = tab[(sm_eff, 1.0)]
+        w = as_frac(p.quota) * 100
+        h = as_frac(sm_eff)
+        w_num.append(w.numerator); w_den.append(w.denominator)
+        h_num.append(h.numerator); h_den.append(h.denominator)
+        if float(sm_eff) != math.floor(float(sm_eff)):
+            integral = False
+        rows[i] = (float(p.sm_partition), float(p.quota), float(thr), area, rpr, float(sm_eff),
+                   (1.0 / rate) if rate > 0 else 0.0, 0, 0, 1 if rate > 0 else 0, 0)
+        key = (-rpr, area, p.sm_partition, p.quota)       # autoscaler.py:94-95
+        if best is None or key < best[0]:
+            best = (key, i)
+    lo = _LoweredProfile(keys, {k: i for i, k in enumerate(keys)}, rows, tuple(w_num),
+                         tuple(w_den), tuple(h_num), tuple(h_den), best[1], integral)
+    if len(_LOWER_CACHE) > 4096:
+        _LOWER_CACHE.clear()
+    _LOWER_CACHE[ckey] = lo
+    return lo
 
 
 @dataclass
@@ -238,14 +296,10 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
     rank = _check_pod_id_order(fids)
     caps = caps or _default_caps(scenario, fns)
 
+    lowered = [_lower_profile(fn.profile, timeshare) for fn in fns]
     # geometry scale: every as_frac(quota)*100 / as_frac(sm_eff) becomes integral
-    wf, hf = [], []
-    for fn in fns:
-        for p in sorted(fn.profile.entries):
-            wf.append(as_frac(p.quota) * 100)
-            hf.append(as_frac(100.0 if timeshare else p.sm_partition))
-    lx = reduce(_lcm, (f.denominator for f in wf), 1)
-    ly = reduce(_lcm, (f.denominator for f in hf), 1)
+    lx = reduce(_lcm, (d for lo in lowered for d in lo.w_den), 1)
+    ly = reduce(_lcm, (d for lo in lowered for d in lo.h_den), 1)
     side_x, side_y = 100 * lx, 100 * ly
     n_nodes = int(scenario.fleet_size)
     if (side_x > _MAX_SIDE or side_y > _MAX_SIDE
@@ -257,50 +311,34 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
     windows = int(scenario.windows)
     n_f = len(fns)
     funcs = np.zeros(n_f, FUNCTION_DT)
-    point_rows, init_rows, point_keys = [], [], []
+    point_blocks, init_rows, point_keys = [], [], []
+    n_points = 0
     counts = np.zeros(n_f * windows, np.int32)
     names = b""
-    sm_integral = True
-    for fi, (fn, tab) in enumerate(zip(fns, tables)):
-        pts = sorted(fn.profile.entries)
-        keys = [(p.sm_partition, p.quota) for p in pts]
-        point_keys.append(keys)
-        index = {k: i for i, k in enumerate(keys)}
-        best = None
-        for i, p in enumerate(pts):
-            e = fn.profile.entries[p]
-            thr = e.throughput_rps
-            area = p.resource_area
-            rpr = thr / area
-            sm_eff = 100.0 if timeshare else p.sm_partition
-            rate = tab[(sm_eff, 1.0)].throughput_rps
-            w = as_frac(p.quota) * 100 * lx
-            h = as_frac(sm_eff) * ly
-            assert w.denominator == 1 and h.denominator == 1
-            if float(sm_eff) != math.floor(float(sm_eff)):
-                sm_integral = False
-            point_rows.append((float(p.sm_partition), float(p.quota), float(thr), area, rpr,
-                               float(sm_eff), (1.0 / rate) if rate > 0 else 0.0,
-                               int(w), int(h), 1 if rate > 0 else 0, 0))
-            key = (-rpr, area, p.sm_partition, p.quota)   # autoscaler.py:94-95
-            if best is None or key < best[0]:
-                best = (key, i)
+    sm_integral = all(lo.sm_integral for lo in lowered)
+    for fi, (fn, lo) in enumerate(zip(fns, lowered)):
+        block = lo.rows.copy()
+        block["rect_w"] = [n * (lx // d) for n, d in zip(lo.w_num, lo.w_den)]
+        block["rect_h"] = [n * (ly // d) for n, d in zip(lo.h_num, lo.h_den)]
+        point_blocks.append(block)
+        point_keys.append(lo.keys)
         for init in fn.initial_pods:
             k = (init.point.sm_partition, init.point.quota)
             has = init.quota_request is not None
-            init_rows.append((index[k], 1 if has else 0,
+            init_rows.append((lo.index[k], 1 if has else 0,
                               float(init.quota_request) if has else 0.0))
         trace = list(fn.trace.counts[:windows])
         counts[fi * windows: fi * windows + len(trace)] = trace
         raw = fn.function_id.encode("utf-8")
         f = funcs[fi]
-        f["n_points"] = len(pts)
-        f["point_off"] = len(point_rows) - len(pts)
+        f["n_points"] = len(lo.keys)
+        f["point_off"] = n_points
+        n_points += len(lo.keys)
         f["n_init"] = len(fn.initial_pods)
         f["init_off"] = len(init_rows) - len(fn.initial_pods)
         f["count_off"] = fi * windows
         f["max_queue"] = -1 if fn.max_queue is None else int(fn.max_queue)
-        f["p_eff"] = best[1]
+        f["p_eff"] = lo.p_eff
         f["id_rank"] = rank[fn.function_id]
         f["name_off"] = len(names)
         f["name_len"] = len(raw)
@@ -332,7 +370,8 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
     s["quantum_s"] = window_s * scenario.quantum
     s["quantum"] = scenario.quantum
     s["capacity_mb"] = scenario.gpu_capacity_mb
-    return RunImage(policy, fids, scen, funcs, np.array(point_rows, POINT_DT),
+    points = np.concatenate(point_blocks) if point_blocks else np.zeros(0, POINT_DT)
+    return RunImage(policy, fids, scen, funcs, points,
                     np.array(init_rows, INIT_DT), counts, names, lx, ly, point_keys)
 
 

@@ -1,0 +1,497 @@
+// gs_kernel.cu -- run driver, kernel entry and the C ABI (include/gshare_b200.h).
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -lineinfo
+//        -Xcompiler -fPIC -shared  (see paper_2309_00558_b200/build.py)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <vector>
+
+#include "gs_kernel.cuh"
+
+namespace gs {
+
+constexpr int MAX_WARPS_PER_BLOCK = 16;
+
+struct Accum {            // per-lane run totals (reduced at the end)
+  long long arrivals, completions, violations, dropped, final_depth;
+};
+
+// ring capacity of bounded queues (sum of max_queue over bounded functions)
+__host__ __device__ inline long long run_ring_total(const gs_scenario_t& sc, const gs_function_t* fs) {
+  long long t = 0;
+  for (int f = 0; f < sc.n_funcs; f++) if (fs[f].max_queue > 0) t += fs[f].max_queue;
+  return t;
+}
+
+__host__ __device__ inline Layout run_layout(const gs_scenario_t& sc, const gs_function_t* fs) {
+  return gs_make_layout(sc.n_nodes, sc.n_funcs, sc.cap_pods, sc.cap_rects, sc.cap_returned,
+                        run_ring_total(sc, fs));
+}
+
+__device__ void init_run(Ctx& c) {
+  for (int i = c.lane; i < c.P; i += 32) {
+    c.p_flags[i] = 0;
+    c.s_free[i] = c.P - 1 - i;  // slot 0 is allocated first
+  }
+  for (int f = c.lane; f < c.F; f += 32) {
+    c.f_qlen[f] = 0; c.f_pinned[f] = 0; c.f_fw[f] = 0; c.f_fi[f] = 0; c.f_fn[f] = 0;
+    c.f_nsn[f] = 0; c.f_nsw[f] = 0; c.f_nsi[f] = 0; c.f_rhead[f] = 0; c.f_retn[f] = 0;
+    c.f_pctr[f] = 0; c.f_warr[f] = 0; c.f_wcomp[f] = 0; c.f_wviol[f] = 0; c.f_wdrop[f] = 0;
+    c.f_hn[f] = 0;
+  }
+  for (int g = c.lane; g < c.G; g += 32) {
+    c.n_sr[g] = 0.0; c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; c.n_fp[g] = 0.0;
+    c.n_nfree[g] = 1; c.n_nres[g] = 0; c.n_nplaced[g] = 0;
+    c.n_rect[g * c.R] = make_int4(0, 0, c.sc->side_x, c.sc->side_y);
+  }
+  for (int i = c.lane; i < c.G * c.F; i += 32) c.n_cnt[i] = 0;
+  if (c.lane == 0) {
+    int off = 0;
+    for (int f = 0; f < c.F; f++) {
+      c.f_ringoff[f] = off;
+      if (c.fs[f].max_queue > 0) off += c.fs[f].max_queue;
+    }
+    WarpShared* s = c.sh;
+    s->n_reg = 0; s->free_top = c.P; s->win_failures = 0; s->n_batch = 0;
+    s->err = 0; s->err_detail = 0; s->err_a0 = 0; s->err_a1 = 0; s->n_list = 0;
+    s->grants = 0; s->decisions = 0; s->attempts = 0; s->frag = 0.0;
+    s->pod_steps = 0; s->rect_scans = 0;
+  }
+  __syncwarp();
+}
+
+__device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PySum& su,
+                             PySum& so, int& peak, int& fail_total) {
+  const gs_scenario_t& sc = *c.sc;
+  for (int f = c.lane; f < c.F; f += 32) {
+    int hn = c.f_hn[f];
+    c.f_hist[3 * f + hn % 3] = (double)c.f_warr[f] / c.ws;   // history.append(n / W)
+    c.f_hn[f] = hn + 1;
+    int depth = c.f_qlen[f] + c.f_fn[f];                      // len(queue) + len(future)
+    if (out.fn_rows) {
+      gs_fn_row_t r;
+      r.arrivals = c.f_warr[f]; r.completions = c.f_wcomp[f]; r.slo_violations = c.f_wviol[f];
+      r.dropped = c.f_wdrop[f]; r.queue_depth = depth;
+      out.fn_rows[sc.fn_row_off + (long long)w * c.F + f] = r;
+    }
+    acc.arrivals += c.f_warr[f]; acc.completions += c.f_wcomp[f];
+    acc.violations += c.f_wviol[f]; acc.dropped += c.f_wdrop[f];
+    if (w == c.W - 1) acc.final_depth += depth;
+    c.f_wcomp[f] = 0; c.f_wviol[f] = 0; c.f_wdrop[f] = 0;
+  }
+  int in_use = 0;
+  for (int g = c.lane; g < c.G; g += 32) {
+    gs_gpu_row_t r;
+    r.present = c.n_nplaced[g] > 0 ? 1 : 0;
+    r.pad = 0;
+    double cov = c.n_cov[g], occ = c.n_occ[g];
+    r.utilization = r.present ? (cov < 1.0 ? cov : 1.0) : 0.0;
+    r.sm_occupancy = r.present ? (occ < 1.0 ? occ : 1.0) : 0.0;
+    r.memory_mb = r.present ? c.n_fp[g] : 0.0;
+    if (out.gpu_rows) out.gpu_rows[sc.gpu_row_off + (long long)w * c.G + g] = r;
+    in_use += r.present;
+  }
+  in_use = warp_sum_i(in_use);
+  __syncwarp();
+  if (c.lane == 0) {
+    for (int g = 0; g < c.G; g++) {           // summary sums in CSV row order
+      if (c.n_nplaced[g] <= 0) continue;
+      double cov = c.n_cov[g], occ = c.n_occ[g];
+      su.add(cov < 1.0 ? cov : 1.0);
+      so.add(occ < 1.0 ? occ : 1.0);
+    }
+    if (out.glob_rows) {
+      gs_glob_row_t r;
+      r.gpus_in_use = in_use;
+      r.placement_failures = c.sh->win_failures;
+      r.fragmentation_index = c.sh->frag;
+      out.glob_rows[sc.glob_row_off + w] = r;
+    }
+    peak = in_use > peak ? in_use : peak;
+    fail_total += c.sh->win_failures;
+    c.sh->win_failures = 0;
+  }
+  __syncwarp();
+}
+
+__device__ void simulate_run(Ctx& c, const gs_out_t& out, int run) {
+  init_run(c);
+  // initial pods: sorted fid order, spec order (sim_engine.py:436-441)
+  if (c.lane == 0) {
+    for (int f = 0; f < c.F && !c.sh->err; f++) {
+      const gs_function_t& fs = c.fs[f];
+      for (int i = 0; i < fs.n_init; i++) {
+        const gs_init_t& ip = c.inits[fs.init_off + i];
+        if (make_pod(c, f, ip.point, ip.has_q_req, ip.q_req, 0) < 0) break;
+      }
+    }
+  }
+  __syncwarp();
+  Accum acc = {0, 0, 0, 0, 0};
+  PySum su, so;
+  su.reset();
+  so.reset();
+  int peak = 0, fail_total = 0;
+  if (!failed(c)) place_batch(c);
+  if (!failed(c)) refresh_frag(c);
+  for (int w = 0; w < c.W && !failed(c); w++) {
+    if (w > 0 && w % c.sc->epoch_windows == 0) {
+      run_epoch(c, w);
+      if (failed(c)) break;
+    }
+    window_begin(c, w);
+    for (int g = c.lane; g < c.G; g += 32) { c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; }
+    __syncwarp();
+    for (int s = 0; s < c.T; s++) {
+      run_step(c, w, s);
+    }
+    complete_tokens(c);
+    window_close(c, w, out, acc, su, so, peak, fail_total);
+  }
+  // outputs
+  gs_status_t st;
+  memset(&st, 0, sizeof(st));
+  int nplaced = 0;
+  if (!c.sh->err) {
+    for (int s0 = 0; s0 < c.P; s0 += 32) {
+      int slot = s0 + c.lane;
+      bool take = slot < c.P && (c.p_flags[slot] & PF_PLACED);
+      unsigned bal = __ballot_sync(FULL, take);
+      if (take && out.placements) {
+        int k = nplaced + __popc(bal & ((1u << c.lane) - 1u));
+        gs_placement_t p;
+        p.node = c.p_node[slot]; p.func = c.p_fn[slot]; p.counter = c.p_ctr[slot];
+        p.x = c.p_x[slot]; p.y = c.p_y[slot]; p.w = c.p_w[slot]; p.h = c.p_h[slot]; p.pad = 0;
+        out.placements[c.sc->place_off + k] = p;
+      }
+      nplaced += __popc(bal);
+    }
+  }
+  acc.arrivals = warp_sum_ll(acc.arrivals);
+  acc.completions = warp_sum_ll(acc.completions);
+  acc.violations = warp_sum_ll(acc.violations);
+  acc.dropped = warp_sum_ll(acc.dropped);
+  acc.final_depth = warp_sum_ll(acc.final_depth);
+  __syncwarp();
+  if (c.lane == 0) {
+    st.code = c.sh->err; st.detail = c.sh->err_detail;
+    st.arg0 = c.sh->err_a0; st.arg1 = c.sh->err_a1;
+    st.n_placements = nplaced;
+    st.token_grants = c.sh->grants;
+    st.scale_decisions = c.sh->decisions;
+    st.placement_attempts = c.sh->attempts;
+    st.pod_steps = c.sh->pod_steps;
+    st.rect_scans = c.sh->rect_scans;
+    out.status[run] = st;
+    if (out.summary) {
+      gs_summary_t sm;
+      sm.windows = c.W; sm.gpus_used_peak = peak; sm.placement_failures = fail_total;
+      sm.n_gpu_rows = su.n;
+      sm.arrivals = acc.arrivals; sm.completions = acc.completions;
+      sm.slo_violations = acc.violations; sm.dropped = acc.dropped;
+      sm.final_queue_depth = acc.final_depth;
+      sm.sum_utilization = su.value(); sm.sum_sm_occupancy = so.value();
+      out.summary[run] = sm;
+    }
+  }
+  __syncwarp();
+}
+
+struct KArgs {
+  gs_batch_t in;              // device pointers
+  gs_out_t out;               // device pointers
+  char* arena;
+  const long long* ws_off;
+  const int* order;
+  int* counter;
+};
+
+__global__ void __launch_bounds__(MAX_WARPS_PER_BLOCK * 32)
+gs_sim_kernel(KArgs a) {
+  __shared__ WarpShared shs[MAX_WARPS_PER_BLOCK];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  WarpShared* sh = &shs[wib];
+  for (;;) {
+    int r = 0;
+    if (lane == 0) r = atomicAdd(a.counter, 1);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= a.in.n_runs) break;
+    const int run = a.order[r];
+    Ctx c;
+    c.sc = &a.in.runs[run];
+    c.fs = &a.in.funcs[c.sc->func_off];
+    c.points = a.in.points;
+    c.counts = a.in.counts;
+    c.inits = a.in.inits;
+    c.G = c.sc->n_nodes; c.F = c.sc->n_funcs; c.P = c.sc->cap_pods; c.R = c.sc->cap_rects;
+    c.RET = c.sc->cap_returned; c.W = c.sc->windows; c.T = c.sc->steps; c.flags = c.sc->flags;
+    c.ws = c.sc->window_s; c.qs = c.sc->quantum_s; c.quantum = c.sc->quantum;
+    c.cap_mb = c.sc->capacity_mb;
+    c.lane = lane;
+    c.sh = sh;
+    Layout L = run_layout(*c.sc, c.fs);
+    ctx_bind(c, a.arena + a.ws_off[run], L);
+    simulate_run(c, a.out, run);
+  }
+}
+
+}  // namespace gs
+
+// ============================================================================
+// C ABI
+// ============================================================================
+using namespace gs;
+
+namespace {
+
+int g_warps_per_block = 4;
+int g_blocks_per_sm = 0;
+
+void put_err(char* err, size_t n, const char* msg) {
+  if (err && n) { std::snprintf(err, n, "%s", msg); }
+}
+
+#define CK(call)                                                               \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      char b_[256];                                                            \
+      std::snprintf(b_, sizeof b_, "%s: %s", #call, cudaGetErrorString(e_));   \
+      put_err(err, err_len, b_);                                               \
+      return GS_ERR_CUDA;                                                      \
+    }                                                                          \
+  } while (0)
+
+template <typename T>
+size_t nbytes(long long n) { return sizeof(T) * (size_t)(n > 0 ? n : 1); }
+
+}  // namespace
+
+struct gs_session {
+  int device = 0;
+  gs_batch_t dev_in{};        // device pointers
+  gs_out_t dev_out{};
+  char* blob = nullptr;       // one allocation for inputs+outputs+arena
+  size_t blob_bytes = 0;
+  long long* ws_off = nullptr;
+  int* order = nullptr;
+  int* counter = nullptr;
+  char* arena = nullptr;
+  int n_runs = 0;
+  int64_t n_fn_rows = 0, n_gpu_rows = 0, n_glob_rows = 0, n_place = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int last_launches = 0;
+  double last_ms = 0.0;
+  size_t input_bytes = 0;
+};
+
+extern "C" int gs_abi_version(void) { return GS_ABI_VERSION; }
+
+extern "C" int gs_set_launch(int warps_per_block, int blocks_per_sm) {
+  if (warps_per_block > 0) g_warps_per_block = std::min(warps_per_block, MAX_WARPS_PER_BLOCK);
+  if (blocks_per_sm >= 0) g_blocks_per_sm = blocks_per_sm;
+  return 0;
+}
+
+extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t** sess_out,
+                                 char* err, size_t err_len) {
+  if (!in || !sess_out || in->n_runs < 0) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
+    put_err(err, err_len, "no CUDA device visible");
+    return GS_ERR_CUDA;
+  }
+  CK(cudaSetDevice(device));
+  gs_session* s = new (std::nothrow) gs_session();
+  if (!s) { put_err(err, err_len, "out of host memory"); return GS_ERR_ARG; }
+  s->device = device;
+  s->n_runs = in->n_runs;
+  s->n_fn_rows = in->n_fn_rows; s->n_gpu_rows = in->n_gpu_rows;
+  s->n_glob_rows = in->n_glob_rows; s->n_place = in->n_placements;
+
+  // per-run workspace offsets + longest-first order (host copies available)
+  const int R = in->n_runs;
+  std::vector<long long> ws_off(R > 0 ? R : 1, 0);
+  std::vector<int> order(R > 0 ? R : 1, 0);
+  std::vector<double> cost(R > 0 ? R : 1, 0.0);
+  long long arena_bytes = 0;
+  for (int r = 0; r < R; r++) {
+    const gs_scenario_t& sc = in->runs[r];
+    if (sc.func_off < 0 || sc.func_off + sc.n_funcs > in->n_funcs || sc.n_nodes < 1 ||
+        sc.cap_pods < 1 || sc.cap_rects < 4 || sc.cap_returned < 1) {
+      put_err(err, err_len, "malformed run record");
+      delete s;
+      return GS_ERR_ARG;
+    }
+    Layout L = run_layout(sc, in->funcs + sc.func_off);
+    ws_off[r] = arena_bytes;
+    arena_bytes += (long long)gs_align16(L.bytes);
+    cost[r] = (double)sc.windows * sc.steps * (sc.n_funcs + sc.n_nodes + 0.25 * sc.cap_pods);
+    order[r] = r;
+  }
+  std::stable_sort(order.begin(), order.begin() + R, [&](int a, int b) { return cost[a] > cost[b]; });
+
+  // one blob: inputs | outputs | ws_off | order | counter | arena
+  size_t off = 0;
+  auto slot = [&](size_t n) { size_t o = off; off = gs_align16(off + n); return o; };
+  size_t o_runs = slot(nbytes<gs_scenario_t>(in->n_runs));
+  size_t o_funcs = slot(nbytes<gs_function_t>(in->n_funcs));
+  size_t o_points = slot(nbytes<gs_point_t>(in->n_points));
+  size_t o_inits = slot(nbytes<gs_init_t>(in->n_inits));
+  size_t o_counts = slot(nbytes<int32_t>(in->n_counts));
+  size_t o_names = slot(nbytes<char>(in->n_names));
+  size_t in_end = off;
+  size_t o_fn = slot(nbytes<gs_fn_row_t>(in->n_fn_rows));
+  size_t o_gpu = slot(nbytes<gs_gpu_row_t>(in->n_gpu_rows));
+  size_t o_glob = slot(nbytes<gs_glob_row_t>(in->n_glob_rows));
+  size_t o_place = slot(nbytes<gs_placement_t>(in->n_placements));
+  size_t o_status = slot(nbytes<gs_status_t>(in->n_runs));
+  size_t o_summary = slot(nbytes<gs_summary_t>(in->n_runs));
+  size_t o_wsoff = slot(nbytes<long long>(R));
+  size_t o_order = slot(nbytes<int>(R));
+  size_t o_counter = slot(sizeof(int));
+  size_t o_arena = slot((size_t)(arena_bytes > 0 ? arena_bytes : 16));
+  s->blob_bytes = off;
+  cudaError_t e = cudaMalloc(&s->blob, s->blob_bytes);
+  if (e != cudaSuccess) {
+    char b[256];
+    std::snprintf(b, sizeof b, "cudaMalloc(%zu bytes): %s", s->blob_bytes, cudaGetErrorString(e));
+    put_err(err, err_len, b);
+    delete s;
+    return GS_ERR_CUDA;
+  }
+  char* B = s->blob;
+  auto up = [&](size_t o, const void* src, size_t n) -> cudaError_t {
+    if (!src || !n) return cudaSuccess;
+    return cudaMemcpy(B + o, src, n, cudaMemcpyHostToDevice);
+  };
+  cudaError_t ce = cudaSuccess;
+  if (ce == cudaSuccess) ce = up(o_runs, in->runs, sizeof(gs_scenario_t) * (size_t)in->n_runs);
+  if (ce == cudaSuccess) ce = up(o_funcs, in->funcs, sizeof(gs_function_t) * (size_t)in->n_funcs);
+  if (ce == cudaSuccess) ce = up(o_points, in->points, sizeof(gs_point_t) * (size_t)in->n_points);
+  if (ce == cudaSuccess) ce = up(o_inits, in->inits, sizeof(gs_init_t) * (size_t)in->n_inits);
+  if (ce == cudaSuccess) ce = up(o_counts, in->counts, sizeof(int32_t) * (size_t)in->n_counts);
+  if (ce == cudaSuccess) ce = up(o_names, in->names, (size_t)in->n_names);
+  if (ce == cudaSuccess) ce = up(o_wsoff, ws_off.data(), sizeof(long long) * (size_t)R);
+  if (ce == cudaSuccess) ce = up(o_order, order.data(), sizeof(int) * (size_t)R);
+  if (ce != cudaSuccess) {
+    put_err(err, err_len, cudaGetErrorString(ce));
+    cudaFree(s->blob);
+    delete s;
+    return GS_ERR_CUDA;
+  }
+  s->input_bytes = in_end;
+  s->dev_in = *in;
+  s->dev_in.runs = reinterpret_cast<const gs_scenario_t*>(B + o_runs);
+  s->dev_in.funcs = reinterpret_cast<const gs_function_t*>(B + o_funcs);
+  s->dev_in.points = reinterpret_cast<const gs_point_t*>(B + o_points);
+  s->dev_in.inits = reinterpret_cast<const gs_init_t*>(B + o_inits);
+  s->dev_in.counts = reinterpret_cast<const int32_t*>(B + o_counts);
+  s->dev_in.names = reinterpret_cast<const char*>(B + o_names);
+  s->dev_out.fn_rows = reinterpret_cast<gs_fn_row_t*>(B + o_fn);
+  s->dev_out.gpu_rows = reinterpret_cast<gs_gpu_row_t*>(B + o_gpu);
+  s->dev_out.glob_rows = reinterpret_cast<gs_glob_row_t*>(B + o_glob);
+  s->dev_out.placements = reinterpret_cast<gs_placement_t*>(B + o_place);
+  s->dev_out.status = reinterpret_cast<gs_status_t*>(B + o_status);
+  s->dev_out.summary = reinterpret_cast<gs_summary_t*>(B + o_summary);
+  s->ws_off = reinterpret_cast<long long*>(B + o_wsoff);
+  s->order = reinterpret_cast<int*>(B + o_order);
+  s->counter = reinterpret_cast<int*>(B + o_counter);
+  s->arena = B + o_arena;
+  cudaEventCreate(&s->ev0);
+  cudaEventCreate(&s->ev1);
+  *sess_out = s;
+  return GS_OK;
+}
+
+extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size_t err_len) {
+  if (!s) { put_err(err, err_len, "null session"); return GS_ERR_ARG; }
+  CK(cudaSetDevice(s->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
+  CK(cudaMemsetAsync(s->counter, 0, sizeof(int), st));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+  const int threads = g_warps_per_block * 32;
+  int per_sm = g_blocks_per_sm;
+  if (per_sm <= 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sim_kernel, threads, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  long long want_warps = (long long)s->n_runs;
+  long long blocks = (long long)sms * per_sm;
+  long long need = (want_warps + g_warps_per_block - 1) / g_warps_per_block;
+  if (need < blocks) blocks = need > 0 ? need : 1;
+  KArgs a;
+  a.in = s->dev_in;
+  a.out = s->dev_out;
+  a.arena = s->arena;
+  a.ws_off = s->ws_off;
+  a.order = s->order;
+  a.counter = s->counter;
+  CK(cudaEventRecord(s->ev0, st));
+  gs_sim_kernel<<<(unsigned)blocks, threads, 0, st>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s->ev1, st));
+  s->last_launches = 1;
+  CK(cudaEventSynchronize(s->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+  s->last_ms = ms;
+  return GS_OK;
+}
+
+extern "C" int gs_session_download(gs_session_t* s, const gs_out_t* out, void* stream_ptr,
+                                   char* err, size_t err_len) {
+  if (!s || !out || !out->status) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
+  CK(cudaSetDevice(s->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
+  auto down = [&](void* dst, const void* src, size_t n) -> cudaError_t {
+    if (!dst || !n) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st);
+  };
+  CK(down(out->fn_rows, s->dev_out.fn_rows, sizeof(gs_fn_row_t) * (size_t)s->n_fn_rows));
+  CK(down(out->gpu_rows, s->dev_out.gpu_rows, sizeof(gs_gpu_row_t) * (size_t)s->n_gpu_rows));
+  CK(down(out->glob_rows, s->dev_out.glob_rows, sizeof(gs_glob_row_t) * (size_t)s->n_glob_rows));
+  CK(down(out->placements, s->dev_out.placements, sizeof(gs_placement_t) * (size_t)s->n_place));
+  CK(down(out->status, s->dev_out.status, sizeof(gs_status_t) * (size_t)s->n_runs));
+  CK(down(out->summary, s->dev_out.summary, sizeof(gs_summary_t) * (size_t)s->n_runs));
+  CK(cudaStreamSynchronize(st));
+  int worst = GS_OK;
+  for (int r = 0; r < s->n_runs; r++) worst = std::max(worst, (int)out->status[r].code);
+  return worst;
+}
+
+extern "C" int gs_session_device_out(gs_session_t* s, gs_out_t* dev_out) {
+  if (!s || !dev_out) return GS_ERR_ARG;
+  *dev_out = s->dev_out;
+  return GS_OK;
+}
+
+extern "C" int gs_session_last_launches(gs_session_t* s) { return s ? s->last_launches : 0; }
+extern "C" double gs_session_last_kernel_ms(gs_session_t* s) { return s ? s->last_ms : 0.0; }
+
+extern "C" void gs_session_destroy(gs_session_t* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev1) cudaEventDestroy(s->ev1);
+  if (s->blob) cudaFree(s->blob);
+  delete s;
+}
+
+extern "C" int gs_run_batch(const gs_batch_t* in, const gs_out_t* out, int device, void* stream,
+                            char* err, size_t err_len) {
+  gs_session_t* s = nullptr;
+  int rc = gs_session_create(in, device, &s, err, err_len);
+  if (rc != GS_OK) return rc;
+  rc = gs_session_run(s, stream, err, err_len);
+  if (rc == GS_OK) rc = gs_session_download(s, out, stream, err, err_len);
+  gs_session_destroy(s);
+  return rc;
+}

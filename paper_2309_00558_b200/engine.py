@@ -21,7 +21,7 @@ from .errors import CapacityError, InvariantError, ValidationError
 from .metrics import FunctionWindowRow, GlobalWindowRow, GpuWindowRow, MetricsReport
 from .scenario import POLICIES
 
-_MAX_CAP_RETRIES = 8
+_MAX_CAP_RETRIES = 16
 
 
 @dataclass
@@ -34,6 +34,9 @@ class RunResult:
     token_grants: int = 0
     scale_decisions: int = 0
     placement_attempts: int = 0
+    summary: object = None          # gs_summary_t record (all-gather payload)
+    pod_steps: int = 0              # registered-pod x quantum-step updates
+    rect_scans: int = 0             # free rectangles examined by best_match
 
     @property
     def decisions(self) -> int:
@@ -85,7 +88,9 @@ def decode_run(batch: cc.Batch, r: int, out: dict) -> RunResult:
     st = out["status"][r]
     res = RunResult(rep, token_grants=int(st["token_grants"]),
                     scale_decisions=int(st["scale_decisions"]),
-                    placement_attempts=int(st["placement_attempts"]))
+                    placement_attempts=int(st["placement_attempts"]),
+                    summary=out["summary"][r].copy(),
+                    pod_steps=int(st["pod_steps"]), rect_scans=int(st["rect_scans"]))
     pl = out["placements"][int(s["place_off"]): int(s["place_off"]) + int(st["n_placements"])]
     nodes: dict = {g: {} for g in range(G)}
     for node, func, counter, x, y, w_, h, _ in pl.tolist():
@@ -107,7 +112,7 @@ def _normalise(scenarios, policies):
 
 
 def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
-             rows: bool = True) -> list:
+             rows: bool = True, caps: cc.Caps | None = None) -> list:
     """Run a batch of (scenario, policy) pairs on the GPU.
 
     Returns one ``RunResult`` per input (or the exception, when
@@ -120,7 +125,7 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
     images: list = [None] * len(scenarios)
     for i, (sc, pol) in enumerate(zip(scenarios, policies)):
         try:
-            images[i] = cc.compile_run(sc, pol)
+            images[i] = cc.compile_run(sc, pol, caps)
         except ValidationError as exc:
             if errors == "raise":
                 raise

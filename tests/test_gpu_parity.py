@@ -1,0 +1,78 @@
+"""GPU parity: the sm_100a kernel, called through the C ABI, against
+(1) the reference's own golden outputs and (2) the CPU oracle at full sizes.
+
+Bit-exact on every record: per-window function rows (arrivals, completions,
+SLO violations, drops, queue depth), GPU rows (utilisation, occupancy,
+memory -- bitwise doubles, i.e. a 0 ulp tolerance, tighter than north_star's
+1e-6 relative), global rows (GPUs in use, placement failures, fragmentation),
+final placements, decision counters and the all-gather summary records.
+"""
+import numpy as np
+import pytest
+
+import golden
+import oracle
+from parity import assert_gpu_matches_oracle, diff_results
+from paper_2309_00558_b200 import backend, compiler as cc, engine, workloads as wl
+from paper_2309_00558_b200.scenario import Scenario
+
+pytestmark = pytest.mark.gpu
+
+
+def _outcomes_on_gpu(recs):
+    scen, pols, pre = [], [], {}
+    for k, rec in enumerate(recs):
+        try:
+            scen.append(golden.load_scenario(rec))
+            pols.append(rec["policy"])
+        except Exception as exc:
+            pre[k] = exc
+    res = engine.simulate(scen, pols, errors="return")
+    it = iter(res)
+    return [pre[k] if k in pre else next(it) for k in range(len(recs))]
+
+
+def test_gpu_matches_reference_golden_runs():
+    recs = golden.records()
+    outcomes = _outcomes_on_gpu(recs)
+    bad = []
+    for rec, out in zip(recs, outcomes):
+        errs = golden.compare(rec, out)
+        if errs:
+            bad.append(f"{rec['name']}/{rec['policy']}: {errs[0][:400]}")
+    assert not bad, f"{len(bad)} of {len(recs)} differ:\n" + "\n".join(bad[:5])
+
+
+@pytest.mark.parametrize("policy", ["fast", "timeshare"])
+def test_gpu_matches_oracle_c2(policy):
+    scen = [Scenario.from_dict(wl.c2(s, windows=120)) for s in range(48)]
+    assert_gpu_matches_oracle(scen, [policy] * len(scen))
+
+
+def test_gpu_matches_oracle_c3_both_policies():
+    scen = [Scenario.from_dict(wl.c3(s)) for s in range(96)]
+    assert_gpu_matches_oracle([x for x in scen for _ in (0, 1)], ["fast", "timeshare"] * 96)
+
+
+def test_gpu_matches_oracle_c5_sweep_sample():
+    scen = [Scenario.from_dict(wl.c5(i)) for i in range(0, 3500, 7)]
+    assert_gpu_matches_oracle(scen, ["fast"] * len(scen))
+
+
+def test_gpu_c1_full_length():
+    sc = Scenario.from_dict(wl.c1())
+    assert_gpu_matches_oracle([sc, sc], ["fast", "timeshare"])
+
+
+def test_capacity_overflow_is_retried_not_truncated():
+    sc = Scenario.from_dict(wl.c2(3, windows=40))
+    tiny = cc.Caps(pods=8, rects=4, returned=1)
+    image = cc.compile_run(sc, "fast", tiny)
+    batch = cc.Batch([image])
+    out = backend.run_batch(batch)
+    assert int(out["status"][0]["code"]) == cc.GS_ERR_CAPACITY
+    # the public API grows the capacities on the device until the run fits
+    res = engine.simulate([sc], ["fast"], caps=tiny)[0]
+    ref_batch = cc.Batch([cc.compile_run(sc, "fast")])
+    want = engine.decode_run(ref_batch, 0, oracle.run_batch(ref_batch))
+    assert diff_results(res, want) == ""

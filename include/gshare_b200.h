@@ -51,7 +51,8 @@ enum {
 };
 
 /* gs_status_t.detail for GS_ERR_CAPACITY */
-enum { GS_CAP_PODS = 1, GS_CAP_RECTS = 2, GS_CAP_RETURNED = 3, GS_CAP_NAMES = 4 };
+enum { GS_CAP_PODS = 1, GS_CAP_RECTS = 2, GS_CAP_RETURNED = 3, GS_CAP_NAMES = 4,
+       GS_CAP_HOT = 5 /* per-window working set outgrew its shared-memory class */ };
 
 /* gs_scenario_t.flags */
 #define GS_FLAG_TIMESHARE   1  /* policy "timeshare": sm_eff = 100 (sim_engine.py:337-338) */
@@ -74,7 +75,7 @@ typedef struct gs_scenario {
   int32_t cap_pods;              /* pod slots (placed + retry + warming)         */
   int32_t cap_rects;             /* free rectangles per node                     */
   int32_t cap_returned;          /* un-pinned-by-removal requests per function   */
-  int32_t pad0;
+  int32_t hot_class;             /* 0 = auto; else minimum shared-memory size class */
   int64_t fn_row_off;            /* windows*n_funcs gs_fn_row_t                  */
   int64_t gpu_row_off;           /* windows*n_nodes gs_gpu_row_t                 */
   int64_t glob_row_off;          /* windows gs_glob_row_t                        */
@@ -154,7 +155,8 @@ typedef struct gs_placement {
 
 typedef struct gs_status {
   int32_t code, detail, arg0, arg1;
-  int32_t n_placements, pad;
+  int32_t n_placements;
+  int32_t hot_class;             /* size class the run executed in (1=S .. 4=XL)  */
   int64_t token_grants;          /* dispatch() outputs, token_backend.py:186     */
   int64_t scale_decisions;       /* len(scale_up)+len(scale_down)                */
   int64_t placement_attempts;    /* best_match calls, sim_engine.py:397          */

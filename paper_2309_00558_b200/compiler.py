@@ -41,14 +41,14 @@ GS_FLAG_SHARING = 2
 GS_FLAG_SM_INTEGRAL = 4
 
 GS_OK, GS_ERR_VALIDATION, GS_ERR_INVARIANT, GS_ERR_CAPACITY, GS_ERR_CUDA, GS_ERR_ARG = range(6)
-GS_CAP_PODS, GS_CAP_RECTS, GS_CAP_RETURNED = 1, 2, 3
+GS_CAP_PODS, GS_CAP_RECTS, GS_CAP_RETURNED, GS_CAP_NAMES, GS_CAP_HOT = 1, 2, 3, 4, 5
 
 SCENARIO_DT = np.dtype([
     ("n_nodes", "<i4"), ("n_funcs", "<i4"), ("windows", "<i4"), ("steps", "<i4"),
     ("epoch_windows", "<i4"), ("cold_start_windows", "<i4"),
     ("restructure_threshold", "<i4"), ("flags", "<i4"), ("func_off", "<i4"),
     ("side_x", "<i4"), ("side_y", "<i4"), ("cap_pods", "<i4"), ("cap_rects", "<i4"),
-    ("cap_returned", "<i4"), ("pad0", "<i4"),
+    ("cap_returned", "<i4"), ("hot_class", "<i4"),
     ("fn_row_off", "<i8"), ("gpu_row_off", "<i8"), ("glob_row_off", "<i8"),
     ("place_off", "<i8"),
     ("window_s", "<f8"), ("quantum_s", "<f8"), ("quantum", "<f8"), ("capacity_mb", "<f8"),
@@ -82,7 +82,7 @@ PLACEMENT_DT = np.dtype([("node", "<i4"), ("func", "<i4"), ("counter", "<i4"),
                          ("x", "<i4"), ("y", "<i4"), ("w", "<i4"), ("h", "<i4"),
                          ("pad", "<i4")], align=True)
 STATUS_DT = np.dtype([("code", "<i4"), ("detail", "<i4"), ("arg0", "<i4"), ("arg1", "<i4"),
-                      ("n_placements", "<i4"), ("pad", "<i4"),
+                      ("n_placements", "<i4"), ("hot_class", "<i4"),
                       ("token_grants", "<i8"), ("scale_decisions", "<i8"),
                       ("placement_attempts", "<i8"), ("pod_steps", "<i8"),
                       ("rect_scans", "<i8")], align=True)
@@ -112,13 +112,17 @@ class Caps:
     pods: int
     rects: int
     returned: int
+    hot_class: int = 0        # 0 = smallest shared-memory class that fits F and G
 
-    def grown(self, detail: int) -> "Caps":
+    def grown(self, detail: int, hot_class_used: int = 0) -> "Caps":
         if detail == GS_CAP_PODS:
-            return Caps(self.pods * 4, self.rects, self.returned)
+            return Caps(self.pods * 4, self.rects, self.returned, self.hot_class)
         if detail == GS_CAP_RECTS:
-            return Caps(self.pods, min(self.rects * 4, _MAX_RECTS_CAP), self.returned)
-        return Caps(self.pods, self.rects, self.returned * 4)
+            return Caps(self.pods, min(self.rects * 4, _MAX_RECTS_CAP), self.returned,
+                        self.hot_class)
+        if detail == GS_CAP_HOT:
+            return Caps(self.pods, self.rects, self.returned, max(self.hot_class, hot_class_used) + 1)
+        return Caps(self.pods, self.rects, self.returned * 4, self.hot_class)
 
 
 @lru_cache(maxsize=65536)
@@ -366,6 +370,7 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
                   | (GS_FLAG_SM_INTEGRAL if sm_integral else 0))
     s["side_x"], s["side_y"] = side_x, side_y
     s["cap_pods"], s["cap_rects"], s["cap_returned"] = caps.pods, caps.rects, caps.returned
+    s["hot_class"] = caps.hot_class
     s["window_s"] = window_s
     s["quantum_s"] = window_s * scenario.quantum
     s["quantum"] = scenario.quantum

@@ -9,9 +9,11 @@
 #include <cstring>
 #include <new>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "gs_kernel.cuh"
+#include "gs_hot.cuh"
 
 namespace gs {
 
@@ -119,7 +121,19 @@ __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PyS
   __syncwarp();
 }
 
-__device__ void simulate_run(Ctx& c, const gs_out_t& out, int run) {
+template <class H> __host__ __device__ constexpr int class_id() {
+  if constexpr (std::is_same<H, HotS>::value) return 1;
+  else if constexpr (std::is_same<H, HotM>::value) return 2;
+  else if constexpr (std::is_same<H, HotL>::value) return 3;
+  else return 4;
+}
+template <class H> __host__ __device__ constexpr size_t hot_bytes() {
+  if constexpr (std::is_void<H>::value) return 0;
+  else return sizeof(H);
+}
+
+template <class H>
+__device__ void simulate_run(Ctx& c, const gs_out_t& out, int run, H* h) {
   init_run(c);
   // initial pods: sorted fid order, spec order (sim_engine.py:436-441)
   if (c.lane == 0) {
@@ -145,12 +159,14 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, int run) {
       if (failed(c)) break;
     }
     window_begin(c, w);
-    for (int g = c.lane; g < c.G; g += 32) { c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; }
-    __syncwarp();
-    for (int s = 0; s < c.T; s++) {
-      run_step(c, w, s);
+    if constexpr (std::is_void<H>::value) {     // XL: working set stays in the HBM arena
+      for (int g = c.lane; g < c.G; g += 32) { c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; }
+      __syncwarp();
+      for (int s = 0; s < c.T; s++) run_step(c, w, s);
+      complete_tokens(c);
+    } else {
+      if (!hot_window(c, h, w)) break;
     }
-    complete_tokens(c);
     window_close(c, w, out, acc, su, so, peak, fail_total);
   }
   // outputs
@@ -182,6 +198,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, int run) {
     st.code = c.sh->err; st.detail = c.sh->err_detail;
     st.arg0 = c.sh->err_a0; st.arg1 = c.sh->err_a1;
     st.n_placements = nplaced;
+    st.hot_class = class_id<H>();
     st.token_grants = c.sh->grants;
     st.scale_decisions = c.sh->decisions;
     st.placement_attempts = c.sh->attempts;
@@ -207,21 +224,25 @@ struct KArgs {
   gs_out_t out;               // device pointers
   char* arena;
   const long long* ws_off;
-  const int* order;
+  const int* order;           // runs of this size class, longest first
+  int n_order;
   int* counter;
 };
 
+template <class H>
 __global__ void __launch_bounds__(MAX_WARPS_PER_BLOCK * 32)
 gs_sim_kernel(KArgs a) {
   __shared__ WarpShared shs[MAX_WARPS_PER_BLOCK];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   WarpShared* sh = &shs[wib];
+  H* hot = reinterpret_cast<H*>(dyn_smem + (size_t)wib * hot_bytes<H>());
   for (;;) {
     int r = 0;
     if (lane == 0) r = atomicAdd(a.counter, 1);
     r = __shfl_sync(FULL, r, 0);
-    if (r >= a.in.n_runs) break;
+    if (r >= a.n_order) break;
     const int run = a.order[r];
     Ctx c;
     c.sc = &a.in.runs[run];
@@ -237,7 +258,7 @@ gs_sim_kernel(KArgs a) {
     c.sh = sh;
     Layout L = run_layout(*c.sc, c.fs);
     ctx_bind(c, a.arena + a.ws_off[run], L);
-    simulate_run(c, a.out, run);
+    simulate_run<H>(c, a.out, run, hot);
   }
 }
 
@@ -273,6 +294,17 @@ size_t nbytes(long long n) { return sizeof(T) * (size_t)(n > 0 ? n : 1); }
 
 }  // namespace
 
+// smallest shared-memory size class whose capacities hold F functions and G
+// nodes (registered pods are checked per window on the device)
+static int run_class(const gs_scenario_t& sc) {
+  int k = 4;
+  if (sc.n_funcs <= HotS::FC && sc.n_nodes <= HotS::GC) k = 1;
+  else if (sc.n_funcs <= HotM::FC && sc.n_nodes <= HotM::GC) k = 2;
+  else if (sc.n_funcs <= HotL::FC && sc.n_nodes <= HotL::GC) k = 3;
+  if (sc.hot_class > k) k = sc.hot_class > 4 ? 4 : sc.hot_class;
+  return k;
+}
+
 struct gs_session {
   int device = 0;
   gs_batch_t dev_in{};        // device pointers
@@ -281,7 +313,8 @@ struct gs_session {
   size_t blob_bytes = 0;
   long long* ws_off = nullptr;
   int* order = nullptr;
-  int* counter = nullptr;
+  int* counter = nullptr;        // one work counter per size class
+  int class_off[6] = {0, 0, 0, 0, 0, 0};  // order[] slice of class k: [off[k-1], off[k])
   char* arena = nullptr;
   int n_runs = 0;
   int64_t n_fn_rows = 0, n_gpu_rows = 0, n_glob_rows = 0, n_place = 0;
@@ -320,6 +353,7 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   std::vector<long long> ws_off(R > 0 ? R : 1, 0);
   std::vector<int> order(R > 0 ? R : 1, 0);
   std::vector<double> cost(R > 0 ? R : 1, 0.0);
+  std::vector<int> cls(R > 0 ? R : 1, 4);
   long long arena_bytes = 0;
   for (int r = 0; r < R; r++) {
     const gs_scenario_t& sc = in->runs[r];
@@ -333,9 +367,17 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
     ws_off[r] = arena_bytes;
     arena_bytes += (long long)gs_align16(L.bytes);
     cost[r] = (double)sc.windows * sc.steps * (sc.n_funcs + sc.n_nodes + 0.25 * sc.cap_pods);
+    cls[r] = run_class(sc);
     order[r] = r;
   }
-  std::stable_sort(order.begin(), order.begin() + R, [&](int a, int b) { return cost[a] > cost[b]; });
+  std::stable_sort(order.begin(), order.begin() + R, [&](int a, int b) {
+    return cls[a] != cls[b] ? cls[a] < cls[b] : cost[a] > cost[b];
+  });
+  for (int k = 1; k <= 4; k++) {
+    int cnt = 0;
+    for (int r = 0; r < R; r++) cnt += cls[r] <= k;
+    s->class_off[k] = cnt;
+  }
 
   // one blob: inputs | outputs | ws_off | order | counter | arena
   size_t off = 0;
@@ -355,7 +397,7 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   size_t o_summary = slot(nbytes<gs_summary_t>(in->n_runs));
   size_t o_wsoff = slot(nbytes<long long>(R));
   size_t o_order = slot(nbytes<int>(R));
-  size_t o_counter = slot(sizeof(int));
+  size_t o_counter = slot(8 * sizeof(int));
   size_t o_arena = slot((size_t)(arena_bytes > 0 ? arena_bytes : 16));
   s->blob_bytes = off;
   cudaError_t e = cudaMalloc(&s->blob, s->blob_bytes);
@@ -410,33 +452,60 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   return GS_OK;
 }
 
+template <class H>
+static int launch_class(const KArgs& a, int sms, cudaStream_t st, char* err, size_t err_len) {
+  const int wpb = g_warps_per_block;
+  const int threads = wpb * 32;
+  const size_t dyn = hot_bytes<H>() * (size_t)wpb;
+  static bool attr_set[8] = {false};
+  if (!attr_set[class_id<H>()]) {
+    CK(cudaFuncSetAttribute(gs_sim_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::max<size_t>(dyn, 48 * 1024)));
+    attr_set[class_id<H>()] = true;
+  }
+  int per_sm = g_blocks_per_sm;
+  if (per_sm <= 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sim_kernel<H>, threads, dyn));
+    if (per_sm < 1) per_sm = 1;
+  }
+  long long blocks = (long long)sms * per_sm;
+  long long need = ((long long)a.n_order + wpb - 1) / wpb;
+  if (need < blocks) blocks = need > 0 ? need : 1;
+  gs_sim_kernel<H><<<(unsigned)blocks, threads, dyn, st>>>(a);
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
 extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size_t err_len) {
   if (!s) { put_err(err, err_len, "null session"); return GS_ERR_ARG; }
   CK(cudaSetDevice(s->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
-  CK(cudaMemsetAsync(s->counter, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(s->counter, 0, 8 * sizeof(int), st));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
-  const int threads = g_warps_per_block * 32;
-  int per_sm = g_blocks_per_sm;
-  if (per_sm <= 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sim_kernel, threads, 0));
-    if (per_sm < 1) per_sm = 1;
-  }
-  long long want_warps = (long long)s->n_runs;
-  long long blocks = (long long)sms * per_sm;
-  long long need = (want_warps + g_warps_per_block - 1) / g_warps_per_block;
-  if (need < blocks) blocks = need > 0 ? need : 1;
-  KArgs a;
-  a.in = s->dev_in;
-  a.out = s->dev_out;
-  a.arena = s->arena;
-  a.ws_off = s->ws_off;
-  a.order = s->order;
-  a.counter = s->counter;
   CK(cudaEventRecord(s->ev0, st));
-  gs_sim_kernel<<<(unsigned)blocks, threads, 0, st>>>(a);
-  CK(cudaGetLastError());
+  s->last_launches = 0;
+  for (int k = 1; k <= 4; k++) {
+    const int lo = s->class_off[k - 1], hi = s->class_off[k];
+    if (hi <= lo) continue;
+    KArgs a;
+    a.in = s->dev_in;
+    a.out = s->dev_out;
+    a.arena = s->arena;
+    a.ws_off = s->ws_off;
+    a.order = s->order + lo;
+    a.n_order = hi - lo;
+    a.counter = s->counter + k;
+    int rc = GS_OK;
+    switch (k) {
+      case 1: rc = launch_class<HotS>(a, sms, st, err, err_len); break;
+      case 2: rc = launch_class<HotM>(a, sms, st, err, err_len); break;
+      case 3: rc = launch_class<HotL>(a, sms, st, err, err_len); break;
+      default: rc = launch_class<void>(a, sms, st, err, err_len); break;
+    }
+    if (rc != GS_OK) return rc;
+    s->last_launches++;
+  }
   CK(cudaEventRecord(s->ev1, st));
   s->last_launches = 1;
   CK(cudaEventSynchronize(s->ev1));

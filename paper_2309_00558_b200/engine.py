@@ -140,8 +140,9 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
         for j, i in enumerate(pending):
             st = out["status"][j]
             if int(st["code"]) == cc.GS_ERR_CAPACITY:
-                caps = cc.Caps(int(batch.runs[j]["cap_pods"]), int(batch.runs[j]["cap_rects"]),
-                               int(batch.runs[j]["cap_returned"])).grown(int(st["detail"]))
+                rr = batch.runs[j]
+                caps = cc.Caps(int(rr["cap_pods"]), int(rr["cap_rects"]), int(rr["cap_returned"]),
+                               int(rr["hot_class"])).grown(int(st["detail"]), int(st["hot_class"]))
                 images[i] = cc.compile_run(scenarios[i], policies[i], caps)
                 retry.append(i)
                 continue

@@ -40,12 +40,34 @@ struct Hot {
   double farr[FC], slo[FC];
   int qlen[FC], pinned[FC], fw[FC], fi[FC], fcnt[FC], nsn[FC], nsw[FC], nsi[FC];
   int rhead[FC], retn[FC], wcomp[FC], wviol[FC], wdrop[FC], maxq[FC], ringoff[FC];
+  int fwn[FC], nswn[FC];   // arrival counts of the cursor windows fw / nsw (cached)
   int loff[FC + 1];
+  int coff[FC];
   // nodes
   double sr[GC], cov[GC], occ[GC];
   int seg[GC + 1];
-  int n;
+  // run constants (so the step loop needs no Ctx registers)
+  const int32_t* counts;
+  long long* f_ret;
+  long long* f_ring;
+  double ws, qs, quantum;
+  int n, F, G, T, W, RET, integral;
   long long grants;
+
+  __device__ __forceinline__ int count(int f, int w) const { return counts[coff[f] + w]; }
+  __device__ __forceinline__ double arrival(int f, int w, int i) const {
+    // start + i * window_s / n, start = window * window_s (sim_engine.py:463,470)
+    return (double)w * ws + ((double)i * ws) / (double)count(f, w);
+  }
+  __device__ __forceinline__ double arrival_n(int w, int i, int n) const {
+    return (double)w * ws + ((double)i * ws) / (double)n;
+  }
+  // next generated request after (w, i); n = count(f, w) is kept in sync
+  __device__ __forceinline__ void advance(int f, int& w, int& i, int& n) const {
+    if (++i < n) return;
+    i = 0;
+    do { w++; n = w < W ? count(f, w) : 1; } while (n == 0);
+  }
 };
 
 // size classes: (pods, functions, nodes)
@@ -94,13 +116,22 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->ringoff[f] = c.f_ringoff[f];
     h->slo[f] = c.fs[f].slo_ms;
     h->farr[f] = h->fcnt[f] > 0 ? arrival_time(c, f, h->fw[f], h->fi[f]) : 0.0;
+    h->fwn[f] = h->fcnt[f] > 0 ? c.count(f, h->fw[f]) : 1;
+    h->nswn[f] = (h->nsn[f] > 0 && c.fs[f].max_queue < 0) ? c.count(f, h->nsw[f]) : 1;
   }
   for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.f_loff[f];
   for (int g = c.lane; g < c.G; g += 32) {
     h->sr[g] = c.n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0;
   }
   for (int g = c.lane; g <= c.G; g += 32) h->seg[g] = c.n_seg[g];
-  if (c.lane == 0) { h->n = n; h->grants = 0; }
+  for (int f = c.lane; f < c.F; f += 32) h->coff[f] = c.fs[f].count_off;
+  if (c.lane == 0) {
+    h->n = n; h->grants = 0;
+    h->counts = c.counts; h->f_ret = c.f_ret; h->f_ring = c.f_ring;
+    h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
+    h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
+    h->integral = c.integral() ? 1 : 0;
+  }
   __syncwarp();
   // s_fl holds arena slots in (node, pod_id) order per function; the hot
   // index of an arena slot is its position in s_rl (slot -> index via s_list).
@@ -139,25 +170,36 @@ __device__ void hot_store(Ctx& c, H* h) {
 }
 
 // ------------------------------------------------------------------- phases
+// The step loop reads everything through `h` (shared memory): no Ctx, so the
+// whole window stays in a handful of registers.
 template <class H>
-__device__ __forceinline__ void hot_complete(const Ctx& c, H* h) {
-  const int n = h->n;
-  if (!c.integral()) {
-    // sm_running -= sm in token (dispatch) order, with the float-dust clamp
-    for (int g = c.lane; g < c.G; g += 32) {
-      double sr = h->sr[g];
-      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
-        int i = h->order[j];
-        if (!(h->flags[i] & PF_GRANT)) break;
-        sr -= h->sm[i];
-        if (sr < 0 && sr > -SM_EPS) sr = 0.0;
-      }
-      h->sr[g] = sr;
+__device__ __forceinline__ void hot_complete_sm(H* h, int lane) {
+  // sm_running -= sm in token (dispatch) order, with the float-dust clamp;
+  // only needed when SM partitions are not integers (else it is exactly 0)
+  #pragma unroll 1
+  for (int g = lane; g < h->G; g += 32) {
+    double sr = h->sr[g];
+    #pragma unroll 1
+    for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+      const int i = h->order[j];
+      if (!(h->flags[i] & PF_GRANT)) break;
+      sr -= h->sm[i];
+      if (sr < 0 && sr > -SM_EPS) sr = 0.0;
     }
+    h->sr[g] = sr;
+  }
+}
+
+template <class H>
+__device__ __forceinline__ void hot_complete(H* h, int lane) {
+  const int n = h->n;
+  if (!h->integral) {
+    hot_complete_sm(h, lane);
     __syncwarp();
   }
-  for (int i = c.lane; i < n; i += 32) {
-    int fl = h->flags[i];
+  #pragma unroll 1
+  for (int i = lane; i < n; i += 32) {
+    const int fl = h->flags[i];
     if (fl & PF_GRANT) {
       h->qused[i] += h->dur[i];
       h->flags[i] = fl & ~PF_GRANT;
@@ -166,80 +208,86 @@ __device__ __forceinline__ void hot_complete(const Ctx& c, H* h) {
 }
 
 template <class H>
-__device__ __forceinline__ void hot_admit(const Ctx& c, H* h, int f, double t0) {
+__device__ __forceinline__ void hot_admit(H* h, int f, double t0) {
   int cnt = h->fcnt[f];
   if (cnt == 0) return;
   double a = h->farr[f];
   const double now = t0 + TIME_EPS;
   if (!(a <= now)) return;
-  int w = h->fw[f], i = h->fi[f];
+  int w = h->fw[f], i = h->fi[f], wn = h->fwn[f];
   const int limit = h->maxq[f];
   int qlen = h->qlen[f], nsn = h->nsn[f], drop = 0;
+  #pragma unroll 1
   while (true) {
-    const int aw = w, ai = i;
+    const int aw = w, ai = i, an = wn;
     cnt--;
-    if (cnt > 0) advance_id(c, f, w, i);
+    if (cnt > 0) h->advance(f, w, i, wn);
     if (limit >= 0 && qlen >= limit) {
       drop++;
     } else {
       qlen++;
       if (limit < 0) {
-        if (nsn == 0) { h->nsw[f] = aw; h->nsi[f] = ai; }
+        if (nsn == 0) { h->nsw[f] = aw; h->nsi[f] = ai; h->nswn[f] = an; }
       } else {
-        c.f_ring[h->ringoff[f] + (h->rhead[f] + nsn) % limit] = pack_id(aw, ai);
+        h->f_ring[h->ringoff[f] + (h->rhead[f] + nsn) % limit] = pack_id(aw, ai);
       }
       nsn++;
     }
     if (cnt == 0) break;
-    a = arrival_time(c, f, w, i);
+    a = h->arrival_n(w, i, wn);
     if (!(a <= now)) break;
   }
   h->farr[f] = a;
-  h->fcnt[f] = cnt; h->fw[f] = w; h->fi[f] = i;
+  h->fcnt[f] = cnt; h->fw[f] = w; h->fi[f] = i; h->fwn[f] = wn;
   h->qlen[f] = qlen; h->nsn[f] = nsn;
   h->wdrop[f] += drop;
 }
 
-// _serve (sim_engine.py:525-552) for hot pod i
+// _serve (sim_engine.py:525-552) for hot pod i of function f
 template <class H>
-__device__ __forceinline__ void hot_serve(const Ctx& c, H* h, int i, int f, double t_start,
-                                          double t_end) {
-  double busy = h->busy[i];
+__device__ __forceinline__ void hot_serve(H* h, int i, int f, double t_start, double t_end) {
+  const double busy = h->busy[i];
   double t = busy > t_start ? busy : t_start;
   if (!(t < t_end - TIME_EPS)) { h->busy[i] = t; return; }
   int fl = h->flags[i];
   double rem = h->crem[i], arr = h->carr[i];
-  const double slo = h->slo[f];
   int comp = 0, viol = 0;
+  #pragma unroll 1
   while (t < t_end - TIME_EPS) {
     if (!(fl & PF_CUR)) {
       long long id;
       const int retn = h->retn[f];
       const int nsn = h->nsn[f];
       if (retn > 0) {               // restarted requests precede never-started ones
-        long long* r = &c.f_ret[(size_t)f * c.RET];
+        long long* r = &h->f_ret[(size_t)f * h->RET];
         id = r[0];
+        #pragma unroll 1
         for (int k = 1; k < retn; k++) r[k - 1] = r[k];
         h->retn[f] = retn - 1;
       } else if (nsn > 0) {
         const int limit = h->maxq[f];
         if (limit < 0) {
-          int nw = h->nsw[f], ni = h->nsi[f];
+          int nw = h->nsw[f], ni = h->nsi[f], nn = h->nswn[f];
           id = pack_id(nw, ni);
-          if (nsn > 1) { advance_id(c, f, nw, ni); h->nsw[f] = nw; h->nsi[f] = ni; }
+          arr = h->arrival_n(nw, ni, nn);
+          if (nsn > 1) {
+            h->advance(f, nw, ni, nn);
+            h->nsw[f] = nw; h->nsi[f] = ni; h->nswn[f] = nn;
+          }
         } else {
           const int hd = h->rhead[f];
-          id = c.f_ring[h->ringoff[f] + hd];
+          id = h->f_ring[h->ringoff[f] + hd];
           h->rhead[f] = (hd + 1) % limit;
+          arr = h->arrival(f, id_w(id), id_i(id));
         }
         h->nsn[f] = nsn - 1;
       } else {
         break;
       }
+      if (retn > 0) arr = h->arrival(f, id_w(id), id_i(id));
       h->pinned[f]++;
       fl |= PF_CUR;
       rem = h->invr[i];
-      arr = arrival_time(c, f, id_w(id), id_i(id));
       h->cur[i] = id;
     }
     const double left = t_end - t;
@@ -251,7 +299,7 @@ __device__ __forceinline__ void hot_serve(const Ctx& c, H* h, int i, int f, doub
       h->pinned[f]--;
       fl &= ~PF_CUR;
       comp++;
-      if ((t - arr) * 1000.0 > slo) viol++;
+      if ((t - arr) * 1000.0 > h->slo[f]) viol++;
     }
   }
   h->busy[i] = t;
@@ -263,28 +311,43 @@ __device__ __forceinline__ void hot_serve(const Ctx& c, H* h, int i, int f, doub
 }
 
 template <class H>
-__device__ void hot_step(const Ctx& c, H* h, int w, int s) {
-  const double t0 = (double)w * c.ws + (double)s * c.qs;
+__device__ void hot_step(H* h, int lane, int w, int s) {
+  const double t0 = (double)w * h->ws + (double)s * h->qs;
   const int n = h->n;
-  if (s > 0) hot_complete(c, h);
-  for (int f = c.lane; f < c.F; f += 32) hot_admit(c, h, f, t0);
+  const int F = h->F, G = h->G;
+  // _admit_arrivals touches only queues and _complete_live_tokens only the
+  // ledger, so admission runs first and completion fuses with the key pass.
+  #pragma unroll 1
+  for (int f = lane; f < F; f += 32) hot_admit(h, f, t0);
+  if (s > 0 && !h->integral) hot_complete_sm(h, lane);
   __syncwarp();
-  // filter_pods + requesting: key = -(q_req - q_used) for requesting pods, ~0 otherwise
-  for (int i = c.lane; i < n; i += 32) {
+  // complete live tokens + filter_pods + requesting:
+  // key = -(q_req - q_used) for requesting pods, ~0 otherwise
+  #pragma unroll 1
+  for (int i = lane; i < n; i += 32) {
     const int f = h->fnode[i] & 0xffff;
-    const double qused = h->qused[i];
+    int fl = h->flags[i];
+    double qused = h->qused[i];
+    if (fl & PF_GRANT) {
+      qused += h->dur[i];
+      h->qused[i] = qused;
+      fl &= ~PF_GRANT;
+      h->flags[i] = fl;
+    }
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
-    const bool req = cand && ((h->flags[i] & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
+    const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
     h->key[i] = req ? ord_key(-(h->qreq[i] - qused)) : ~0ull;
   }
   __syncwarp();
   // build_queue order inside each node by rank counting: (key, pod_id), and
   // pod_id order == hot index order within a node
-  for (int i = c.lane; i < n; i += 32) {
+  #pragma unroll 1
+  for (int i = lane; i < n; i += 32) {
     const int g = h->fnode[i] >> 16;
     const unsigned long long k = h->key[i];
     const int lo = h->seg[g], hi = h->seg[g + 1];
     int r = 0;
+    #pragma unroll 1
     for (int j = lo; j < hi; j++) {
       const unsigned long long kj = h->key[j];
       r += (kj < k) || (kj == k && j < i);
@@ -294,19 +357,23 @@ __device__ void hot_step(const Ctx& c, H* h, int w, int s) {
   __syncwarp();
   // dispatch (head-blocking) + coverage/occupancy, one lane per node
   int grants = 0;
-  for (int g = c.lane; g < c.G; g += 32) {
-    double sr = c.integral() ? 0.0 : h->sr[g];
+  const double quantum = h->quantum;
+  #pragma unroll 1
+  for (int g = lane; g < G; g += 32) {
+    double sr = h->integral ? 0.0 : h->sr[g];
     double mx = 0.0;
     PySum occ;
     occ.reset();
     int ng = 0;
-    for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+    const int e = h->seg[g + 1];
+    #pragma unroll 1
+    for (int j = h->seg[g]; j < e; j++) {
       const int i = h->order[j];
       if (h->key[i] == ~0ull) break;          // rest of the node is not requesting
       const double sm = h->sm[i];
       if (sm + sr > SM_LIMIT + SM_EPS) break;
       const double rem = h->qlim[i] - h->qused[i];
-      const double dur = rem < c.quantum ? rem : c.quantum;
+      const double dur = rem < quantum ? rem : quantum;
       h->dur[i] = dur;
       h->flags[i] |= PF_GRANT;
       sr += sm;
@@ -314,7 +381,7 @@ __device__ void hot_step(const Ctx& c, H* h, int w, int s) {
       occ.add(sm * dur);
       ng++;
     }
-    if (!c.integral()) h->sr[g] = sr;
+    if (!h->integral) h->sr[g] = sr;
     if (ng) {
       h->cov[g] += mx;
       h->occ[g] += occ.value() / 100.0;
@@ -322,25 +389,35 @@ __device__ void hot_step(const Ctx& c, H* h, int w, int s) {
     grants += ng;
   }
   grants = warp_sum_i(grants);
-  if (c.lane == 0) h->grants += grants;
+  if (lane == 0) h->grants += grants;
   __syncwarp();
   // serve, per function in (node, pod_id) order
-  for (int f = c.lane; f < c.F; f += 32) {
+  const double ws = h->ws;
+  #pragma unroll 1
+  for (int f = lane; f < F; f += 32) {
     const int e = h->loff[f + 1];
+    #pragma unroll 1
     for (int j = h->loff[f]; j < e; j++) {
       const int i = h->flist[j];
-      if (h->flags[i] & PF_GRANT) hot_serve(c, h, i, f, t0, t0 + h->dur[i] * c.ws);
+      if (h->flags[i] & PF_GRANT) hot_serve(h, i, f, t0, t0 + h->dur[i] * ws);
     }
   }
   __syncwarp();
 }
 
 template <class H>
+__device__ __noinline__ void hot_steps(H* h, int lane, int w) {
+  const int T = h->T;
+  #pragma unroll 1
+  for (int s = 0; s < T; s++) hot_step(h, lane, w, s);
+  hot_complete(h, lane);
+  __syncwarp();
+}
+
+template <class H>
 __device__ bool hot_window(Ctx& c, H* h, int w) {
   if (!hot_load(c, h)) return false;
-  for (int s = 0; s < c.T; s++) hot_step(c, h, w, s);
-  hot_complete(c, h);
-  __syncwarp();
+  hot_steps(h, c.lane, w);
   hot_store(c, h);
   return true;
 }

@@ -17,7 +17,7 @@
 
 namespace gs {
 
-constexpr int MAX_WARPS_PER_BLOCK = 16;
+constexpr int MAX_WARPS_PER_BLOCK = 4;   // launch bounds: 128 threads x 6 blocks/SM
 
 struct Accum {            // per-lane run totals (reduced at the end)
   long long arrivals, completions, violations, dropped, final_depth;
@@ -230,7 +230,7 @@ struct KArgs {
 };
 
 template <class H>
-__global__ void __launch_bounds__(MAX_WARPS_PER_BLOCK * 32)
+__global__ void __launch_bounds__(128, 6)
 gs_sim_kernel(KArgs a) {
   __shared__ WarpShared shs[MAX_WARPS_PER_BLOCK];
   extern __shared__ __align__(16) unsigned char dyn_smem[];

@@ -632,12 +632,28 @@ __device__ void place_batch(Ctx& c) {
   warp_sort(c, nb);
   for (int i = c.lane; i < nb; i += 32) c.s_batch[i] = c.s_ki[i];
   __syncwarp();
+  // best_match is a pure function of (node state, function, w, h): once a
+  // request fails, identical requests fail too until a placement changes the
+  // state, so they are answered from a one-entry memo (same counters).
+  int memo_f = -1, memo_w = 0, memo_h = 0;
+  long long memo_scans = 0;
   for (int i = 0; i < nb; i++) {
     int slot = c.s_batch[i];
+    int f = c.p_fn[slot], pw = c.p_w[slot], ph = c.p_h[slot];
     int4 chosen;
-    int g = best_match(c, slot, &chosen);
+    int g;
+    if (f == memo_f && pw == memo_w && ph == memo_h) {
+      g = -1;
+      if (c.lane == 0) c.sh->rect_scans += memo_scans;
+    } else {
+      long long before = c.sh->rect_scans;
+      g = best_match(c, slot, &chosen);
+      __syncwarp();
+      memo_scans = c.sh->rect_scans - before;
+    }
     if (c.lane == 0) c.sh->attempts++;
     if (g < 0) {
+      memo_f = f; memo_w = pw; memo_h = ph;
       if (c.lane == 0) {
         c.sh->win_failures++;
         c.p_flags[slot] |= PF_RETRY;
@@ -645,6 +661,7 @@ __device__ void place_batch(Ctx& c) {
       __syncwarp();
       continue;
     }
+    memo_f = -1;
     if (!place_pod(c, slot, g, chosen)) return;
   }
   __syncwarp();

@@ -35,17 +35,20 @@ struct Hot {
   unsigned long long key[PC];
   long long cur[PC];
   int slot[PC], fnode[PC], flags[PC];
-  short order[PC], flist[PC];
+  short order[PC], flist[PC], rank[PC], gl[PC];
   // functions
   double farr[FC], slo[FC];
   int qlen[FC], pinned[FC], fw[FC], fi[FC], fcnt[FC], nsn[FC], nsw[FC], nsi[FC];
   int rhead[FC], retn[FC], wcomp[FC], wviol[FC], wdrop[FC], maxq[FC], ringoff[FC];
   int fwn[FC], nswn[FC];   // arrival counts of the cursor windows fw / nsw (cached)
+  int favail[FC], fcarry[FC], fcomp[FC], fviol[FC];   // parallel-serve scratch
   int loff[FC + 1];
   int coff[FC];
   // nodes
   double sr[GC], cov[GC], occ[GC];
   int seg[GC + 1];
+  int cut[GC];
+  unsigned long long covbits[GC];
   // run constants (so the step loop needs no Ctx registers)
   const int32_t* counts;
   long long* f_ret;
@@ -310,20 +313,111 @@ __device__ __forceinline__ void hot_serve(H* h, int i, int f, double t_start, do
   h->wviol[f] += viol;
 }
 
+// id of the `pos`-th unpinned request of function f at the start of the serve
+// phase: restarted (returned) requests first, then never-started ones in
+// queue order (sim_engine.py:531 takes the first request with server None).
+template <class H>
+__device__ __forceinline__ double unpinned_at(const H* h, int f, int pos, long long* id_out) {
+  const int retn = h->retn[f];
+  if (pos < retn) {
+    const long long id = h->f_ret[(size_t)f * h->RET + pos];
+    *id_out = id;
+    return h->arrival(f, id_w(id), id_i(id));
+  }
+  const int q = pos - retn;
+  const int limit = h->maxq[f];
+  if (limit >= 0) {
+    const long long id = h->f_ring[h->ringoff[f] + (h->rhead[f] + q) % limit];
+    *id_out = id;
+    return h->arrival(f, id_w(id), id_i(id));
+  }
+  int w = h->nsw[f], i = h->nsi[f] + q, n = h->nswn[f];
+  while (i >= n) {
+    i -= n;
+    do { w++; n = h->count(f, w); } while (n == 0);
+  }
+  *id_out = pack_id(w, i);
+  return h->arrival_n(w, i, n);
+}
+
+// How many requests pod i would start in [t_start, t_end) if the queue never
+// ran dry (the serve loop's timing does not depend on which request it gets).
+template <class H>
+__device__ __forceinline__ int serve_dry_run(const H* h, int i, double t_start, double t_end) {
+  const double busy = h->busy[i];
+  double t = busy > t_start ? busy : t_start;
+  bool cur = (h->flags[i] & PF_CUR) != 0;
+  double rem = h->crem[i];
+  const double inv = h->invr[i];
+  int picks = 0;
+#pragma unroll 1
+  while (t < t_end - TIME_EPS) {
+    if (!cur) { picks++; cur = true; rem = inv; }
+    const double left = t_end - t;
+    const double span = rem < left ? rem : left;
+    rem -= span;
+    t += span;
+    if (rem <= TIME_EPS) cur = false;
+  }
+  return picks;
+}
+
+// _serve (sim_engine.py:525-552) for pod i whose k-th new request is the
+// (base+k)-th unpinned one and which may start at most `avail` requests.
+template <class H>
+__device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start, double t_end,
+                                             int base, int avail, int& comp, int& viol) {
+  const double busy = h->busy[i];
+  double t = busy > t_start ? busy : t_start;
+  if (!(t < t_end - TIME_EPS)) { h->busy[i] = t; return; }
+  int fl = h->flags[i];
+  double rem = h->crem[i], arr = h->carr[i];
+  const double slo = h->slo[f];
+  int taken = 0;
+#pragma unroll 1
+  while (t < t_end - TIME_EPS) {
+    if (!(fl & PF_CUR)) {
+      if (taken == avail) break;                 // queue ran dry
+      long long id;
+      arr = unpinned_at(h, f, base + taken, &id);
+      taken++;
+      h->cur[i] = id;
+      rem = h->invr[i];
+      fl |= PF_CUR;
+    }
+    const double left = t_end - t;
+    const double span = rem < left ? rem : left;
+    rem -= span;
+    t += span;
+    if (rem <= TIME_EPS) {
+      fl &= ~PF_CUR;
+      comp++;
+      if ((t - arr) * 1000.0 > slo) viol++;
+    }
+  }
+  h->busy[i] = t;
+  h->crem[i] = rem;
+  h->carr[i] = arr;
+  h->flags[i] = fl;
+}
+
 template <class H>
 __device__ void hot_step(H* h, int lane, int w, int s) {
   const double t0 = (double)w * h->ws + (double)s * h->qs;
   const int n = h->n;
   const int F = h->F, G = h->G;
+  const bool integral = h->integral != 0;
   // _admit_arrivals touches only queues and _complete_live_tokens only the
   // ledger, so admission runs first and completion fuses with the key pass.
-  #pragma unroll 1
+#pragma unroll 1
   for (int f = lane; f < F; f += 32) hot_admit(h, f, t0);
-  if (s > 0 && !h->integral) hot_complete_sm(h, lane);
+  if (s > 0 && !integral) hot_complete_sm(h, lane);
+#pragma unroll 1
+  for (int g = lane; g < G; g += 32) { h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull; }
   __syncwarp();
   // complete live tokens + filter_pods + requesting:
   // key = -(q_req - q_used) for requesting pods, ~0 otherwise
-  #pragma unroll 1
+#pragma unroll 1
   for (int i = lane; i < n; i += 32) {
     const int f = h->fnode[i] & 0xffff;
     int fl = h->flags[i];
@@ -339,68 +433,186 @@ __device__ void hot_step(H* h, int lane, int w, int s) {
     h->key[i] = req ? ord_key(-(h->qreq[i] - qused)) : ~0ull;
   }
   __syncwarp();
-  // build_queue order inside each node by rank counting: (key, pod_id), and
-  // pod_id order == hot index order within a node
-  #pragma unroll 1
+  // build_queue order inside each node by rank counting on (key, pod_id)
+  // (pod_id order == hot index order within a node).  With integral SM
+  // partitions the running SM sum is exact in any order, so dispatch's
+  // head-blocking cut is decided here too: a requesting pod misfits iff
+  // sm + (SM of the requesting pods ahead of it) > 100 + 1e-9, and the node's
+  // cut is the smallest misfit rank (token_backend.py:169-177).
+#pragma unroll 1
   for (int i = lane; i < n; i += 32) {
     const int g = h->fnode[i] >> 16;
     const unsigned long long k = h->key[i];
     const int lo = h->seg[g], hi = h->seg[g + 1];
     int r = 0;
-    #pragma unroll 1
+    double ahead = 0.0;
+#pragma unroll 1
     for (int j = lo; j < hi; j++) {
       const unsigned long long kj = h->key[j];
-      r += (kj < k) || (kj == k && j < i);
+      const bool less = (kj < k) || (kj == k && j < i);
+      r += less;
+      if (less) ahead += h->sm[j];
     }
     h->order[lo + r] = (short)i;
+    h->rank[i] = (short)r;
+    if (integral && k != ~0ull && h->sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], r);
   }
   __syncwarp();
-  // dispatch (head-blocking) + coverage/occupancy, one lane per node
-  int grants = 0;
   const double quantum = h->quantum;
-  #pragma unroll 1
-  for (int g = lane; g < G; g += 32) {
-    double sr = h->integral ? 0.0 : h->sr[g];
-    double mx = 0.0;
-    PySum occ;
-    occ.reset();
-    int ng = 0;
-    const int e = h->seg[g + 1];
-    #pragma unroll 1
-    for (int j = h->seg[g]; j < e; j++) {
-      const int i = h->order[j];
-      if (h->key[i] == ~0ull) break;          // rest of the node is not requesting
-      const double sm = h->sm[i];
-      if (sm + sr > SM_LIMIT + SM_EPS) break;
-      const double rem = h->qlim[i] - h->qused[i];
-      const double dur = rem < quantum ? rem : quantum;
-      h->dur[i] = dur;
-      h->flags[i] |= PF_GRANT;
-      sr += sm;
-      if (ng == 0 || dur > mx) mx = dur;
-      occ.add(sm * dur);
-      ng++;
+  int grants = 0;
+  if (integral) {
+#pragma unroll 1
+    for (int i = lane; i < n; i += 32) {
+      const int g = h->fnode[i] >> 16;
+      if (h->key[i] != ~0ull && h->rank[i] < h->cut[g]) {
+        const double rem = h->qlim[i] - h->qused[i];
+        const double dur = rem < quantum ? rem : quantum;
+        h->dur[i] = dur;
+        h->flags[i] |= PF_GRANT;
+        atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
+        grants++;
+      }
     }
-    if (!h->integral) h->sr[g] = sr;
-    if (ng) {
-      h->cov[g] += mx;
-      h->occ[g] += occ.value() / 100.0;
+    __syncwarp();
+    // occupancy: Python sum() of sm*duration in dispatch order, per node
+#pragma unroll 1
+    for (int g = lane; g < G; g += 32) {
+      PySum occ;
+      occ.reset();
+      const int e = h->seg[g + 1];
+#pragma unroll 1
+      for (int j = h->seg[g]; j < e; j++) {
+        const int i = h->order[j];
+        if (!(h->flags[i] & PF_GRANT)) break;
+        occ.add(h->sm[i] * h->dur[i]);
+      }
+      if (occ.n) {
+        h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
+        h->occ[g] += occ.value() / 100.0;
+      }
     }
-    grants += ng;
+  } else {
+    // general case: sequential head-blocking walk with the float sm_running
+#pragma unroll 1
+    for (int g = lane; g < G; g += 32) {
+      double sr = h->sr[g];
+      double mx = 0.0;
+      PySum occ;
+      occ.reset();
+      int ng = 0;
+      const int e = h->seg[g + 1];
+#pragma unroll 1
+      for (int j = h->seg[g]; j < e; j++) {
+        const int i = h->order[j];
+        if (h->key[i] == ~0ull) break;          // rest of the node is not requesting
+        const double sm = h->sm[i];
+        if (sm + sr > SM_LIMIT + SM_EPS) break;
+        const double rem = h->qlim[i] - h->qused[i];
+        const double dur = rem < quantum ? rem : quantum;
+        h->dur[i] = dur;
+        h->flags[i] |= PF_GRANT;
+        sr += sm;
+        if (ng == 0 || dur > mx) mx = dur;
+        occ.add(sm * dur);
+        ng++;
+      }
+      h->sr[g] = sr;
+      if (ng) {
+        h->cov[g] += mx;
+        h->occ[g] += occ.value() / 100.0;
+      }
+      grants += ng;
+    }
   }
   grants = warp_sum_i(grants);
   if (lane == 0) h->grants += grants;
-  __syncwarp();
-  // serve, per function in (node, pod_id) order
-  const double ws = h->ws;
-  #pragma unroll 1
+  // serve (sim_engine.py:514-520), pod-parallel.  Granted pods in (function,
+  // node, pod_id) order; a dry run counts each pod's request starts, a
+  // segmented scan per function turns them into FIFO positions, and a replay
+  // serves exactly the requests the sequential drain would have handed out.
+#pragma unroll 1
   for (int f = lane; f < F; f += 32) {
-    const int e = h->loff[f + 1];
-    #pragma unroll 1
-    for (int j = h->loff[f]; j < e; j++) {
-      const int i = h->flist[j];
-      if (h->flags[i] & PF_GRANT) hot_serve(h, i, f, t0, t0 + h->dur[i] * ws);
+    h->favail[f] = h->retn[f] + h->nsn[f];
+    h->fcarry[f] = 0; h->fcomp[f] = 0; h->fviol[f] = 0;
+  }
+  __syncwarp();
+  int ngl = 0;
+#pragma unroll 1
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int j = j0 + lane;
+    const int i = j < n ? h->flist[j] : 0;
+    const bool gr = j < n && (h->flags[i] & PF_GRANT);
+    const unsigned bal = __ballot_sync(FULL, gr);
+    if (gr) h->gl[ngl + __popc(bal & ((1u << lane) - 1u))] = (short)i;
+    ngl += __popc(bal);
+  }
+  __syncwarp();
+  const double ws = h->ws;
+#pragma unroll 1
+  for (int k0 = 0; k0 < ngl; k0 += 32) {
+    const int k = k0 + lane;
+    const bool act = k < ngl;
+    const int i = act ? h->gl[k] : 0;
+    const int f = act ? (h->fnode[i] & 0xffff) : -1 - lane;
+    const double t_end = t0 + h->dur[i] * ws;
+    const int picks = act ? serve_dry_run(h, i, t0, t_end) : 0;
+    int v = picks;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, v, o);
+      const int fo = __shfl_up_sync(FULL, f, o);
+      if (lane >= o && fo == f) v += y;
     }
+    const int fnext = __shfl_down_sync(FULL, f, 1);
+    const bool seg_end = act && (lane == 31 || k + 1 >= ngl || fnext != f);
+    if (act) {
+      const int base = h->fcarry[f] + v - picks;
+      int avail = h->favail[f] - base;
+      avail = avail < 0 ? 0 : (avail > picks ? picks : avail);
+      int comp = 0, viol = 0;
+      serve_replay(h, i, f, t0, t_end, base, avail, comp, viol);
+      if (comp) atomicAdd(&h->fcomp[f], comp);
+      if (viol) atomicAdd(&h->fviol[f], viol);
+    }
+    __syncwarp();
+    if (seg_end) h->fcarry[f] += v;
+    __syncwarp();
+  }
+  // apply each function's queue bookkeeping once
+#pragma unroll 1
+  for (int f = lane; f < F; f += 32) {
+    const int want = h->fcarry[f];
+    if (want == 0 && h->fcomp[f] == 0) continue;
+    const int avail = h->favail[f];
+    const int taken = want < avail ? want : avail;
+    const int retn = h->retn[f];
+    const int from_ret = taken < retn ? taken : retn;
+    const int from_ns = taken - from_ret;
+    if (from_ret) {
+      long long* r = &h->f_ret[(size_t)f * h->RET];
+      for (int q = from_ret; q < retn; q++) r[q - from_ret] = r[q];
+      h->retn[f] = retn - from_ret;
+    }
+    if (from_ns) {
+      const int nsn = h->nsn[f] - from_ns;
+      h->nsn[f] = nsn;
+      const int limit = h->maxq[f];
+      if (limit >= 0) {
+        h->rhead[f] = (h->rhead[f] + from_ns) % limit;
+      } else if (nsn > 0) {
+        int w2 = h->nsw[f], i2 = h->nsi[f] + from_ns, n2 = h->nswn[f];
+        while (i2 >= n2) {
+          i2 -= n2;
+          do { w2++; n2 = h->count(f, w2); } while (n2 == 0);
+        }
+        h->nsw[f] = w2; h->nsi[f] = i2; h->nswn[f] = n2;
+      }
+    }
+    const int comp = h->fcomp[f];
+    h->pinned[f] += taken - comp;
+    h->qlen[f] -= comp;
+    h->wcomp[f] += comp;
+    h->wviol[f] += h->fviol[f];
   }
   __syncwarp();
 }

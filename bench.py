@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("cuda", "reference"), default="cuda")
-    ap.add_argument("--runs", type=int, default=4736, help="scenario runs per GPU")
+    ap.add_argument("--runs", type=int, default=9472, help="scenario runs per GPU")
     ap.add_argument("--windows", type=int, default=300)
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="runs in the CPU baseline sample (0 = auto)")
@@ -155,6 +155,11 @@ def cpu_reference(batch, sample_runs: int, threads: int):
     return sim_seconds(sub) / dt, dt, sub
 
 
+def fleet_totals(summary):
+    from paper_2309_00558_b200.dist import summary_totals
+    return summary_totals(summary)
+
+
 def load_peak():
     try:
         with open(PEAKS) as fh:
@@ -259,12 +264,12 @@ def main():
 
     # NCCL all-gather of the fixed-size per-run summary records
     summ = out["summary"]
-    gathered_runs = len(summ)
+    fleet = summ
     if dist is not None:
-        raw = torch.from_numpy(summ.view(np.uint8).copy()).cuda()
-        allb = torch.empty(raw.numel() * world, dtype=torch.uint8, device="cuda")
-        dist.all_gather_into_tensor(allb, raw)
-        gathered_runs = allb.numel() // summ.itemsize
+        from paper_2309_00558_b200 import dist as gdist
+        fleet = gdist.all_gather_summaries(summ, args.runs * world,
+                                           device=torch.device("cuda", local))
+    gathered_runs = len(fleet)
     sim_s = sim_seconds(batch) * world
     value = sim_s / (total_ms / 1000.0 / args.steps)
     st = out["status"]
@@ -304,6 +309,7 @@ def main():
             "config": {"workload": WORKLOAD, "runs_per_gpu": args.runs, "windows": args.windows,
                        "policy": "fast", "l2": "flushed between launches (256 MiB write)",
                        "failed_runs": bad, "summaries_all_gathered": gathered_runs},
+            "fleet_summary": fleet_totals(fleet),
             "decisions_per_sec": dec_per_s,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

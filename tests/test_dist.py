@@ -1,0 +1,64 @@
+"""Multi-process host logic on CPU: world_size-2 gloo.
+
+The scenario shard of each rank plus one all-gather of the per-run summary
+records must reassemble exactly the single-process result.  The summaries
+are produced by the CPU oracle here (no GPU in this container); on a GPU box
+the same code path runs with NCCL on device buffers (bench.py, dist.py).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2309_00558_b200 import compiler as cc, dist as gd, workloads as wl
+
+
+def test_shard_is_a_balanced_partition():
+    for n in (0, 1, 7, 64, 4737):
+        for world in (1, 2, 3, 8):
+            parts = [gd.shard(n, r, world) for r in range(world)]
+            flat = [i for p in parts for i in p]
+            assert flat == list(range(n))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, n_runs, out_dir):
+    import sys
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    scen = wl.c2_scenarios(range(n_runs), windows=40)
+    mine = gd.shard(n_runs, rank, world)
+    batch = cc.Batch([cc.compile_run(scen[i], "fast") for i in mine])
+    local = oracle.run_batch(batch, rows=False)["summary"]
+    gathered = gd.all_gather_summaries(local, n_runs)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "gathered.npy"), gathered)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_all_gather_reassembles_the_batch(tmp_path):
+    import oracle
+    n_runs = 13
+    mp.spawn(_worker, args=(2, _free_port(), n_runs, str(tmp_path)), nprocs=2, join=True)
+    gathered = np.load(tmp_path / "gathered.npy")
+    scen = wl.c2_scenarios(range(n_runs), windows=40)
+    whole = oracle.run_batch(cc.Batch([cc.compile_run(s, "fast") for s in scen]),
+                             rows=False)["summary"]
+    assert gathered.tobytes() == whole.tobytes()
+    tot = gd.summary_totals(gathered)
+    assert tot["runs"] == n_runs and tot["arrivals"] > 0

@@ -162,6 +162,7 @@ typedef struct gs_status {
   int64_t placement_attempts;    /* best_match calls, sim_engine.py:397          */
   int64_t pod_steps;             /* sum over quantum steps of registered pods    */
   int64_t rect_scans;            /* free rects examined by best_match            */
+  int64_t peak_pods;             /* most pods alive at once (capacity sizing)    */
 } gs_status_t;
 
 /* Fixed-size per-run record all-gathered across GPUs (metrics.py:94-131). */

@@ -77,7 +77,7 @@ typedef struct {
   Node* nodes;
   int* retry; int nretry, cretry;
   int win_failures;
-  long long grants, decisions, attempts, pod_steps, rect_scans;
+  long long grants, decisions, attempts, pod_steps, rect_scans, peak_pods;
   int err_code, err_fn, err_pt;
 } Eng;
 
@@ -302,6 +302,11 @@ static int make_pod(Eng* e, int f, int k, int has_qreq, double q_req, int warm_a
   p->rw = pt->rect_w; p->rh = pt->rect_h;
   p->inv_rate = pt->inv_rate;
   p->gpu = -1; p->warm_at = warm_at;
+  {
+    long long alive = 0;
+    for (int i = 0; i < e->npods; i++) alive += e->pods[i].alive;
+    if (alive > e->peak_pods) e->peak_pods = alive;
+  }
   return slot;
 }
 
@@ -736,6 +741,7 @@ done:
   st->placement_attempts = e->attempts;
   st->pod_steps = e->pod_steps;
   st->rect_scans = e->rect_scans;
+  st->peak_pods = e->peak_pods;
   if (out->summary) out->summary[run] = sum;
   free_engine(e);
   return st->code;

@@ -85,7 +85,7 @@ STATUS_DT = np.dtype([("code", "<i4"), ("detail", "<i4"), ("arg0", "<i4"), ("arg
                       ("n_placements", "<i4"), ("hot_class", "<i4"),
                       ("token_grants", "<i8"), ("scale_decisions", "<i8"),
                       ("placement_attempts", "<i8"), ("pod_steps", "<i8"),
-                      ("rect_scans", "<i8")], align=True)
+                      ("rect_scans", "<i8"), ("peak_pods", "<i8")], align=True)
 SUMMARY_DT = np.dtype([("windows", "<i4"), ("gpus_used_peak", "<i4"),
                        ("placement_failures", "<i4"), ("n_gpu_rows", "<i4"),
                        ("arrivals", "<i8"), ("completions", "<i8"),

@@ -42,6 +42,8 @@ struct Hot {
   int rhead[FC], retn[FC], wcomp[FC], wviol[FC], wdrop[FC], maxq[FC], ringoff[FC];
   int fwn[FC], nswn[FC];   // arrival counts of the cursor windows fw / nsw (cached)
   int favail[FC], fcarry[FC], fcomp[FC], fviol[FC];   // parallel-serve scratch
+  int warr[FC], hn[FC];
+  double hist[3 * FC];
   int loff[FC + 1];
   int coff[FC];
   // nodes
@@ -49,13 +51,14 @@ struct Hot {
   int seg[GC + 1];
   int cut[GC];
   unsigned long long covbits[GC];
+  int nplaced[GC];
+  double fp[GC];
   // run constants (so the step loop needs no Ctx registers)
   const int32_t* counts;
   long long* f_ret;
   long long* f_ring;
   double ws, qs, quantum;
   int n, F, G, T, W, RET, integral;
-  long long grants;
 
   __device__ __forceinline__ int count(int f, int w) const { return counts[coff[f] + w]; }
   __device__ __forceinline__ double arrival(int f, int w, int i) const {
@@ -115,6 +118,9 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->nsn[f] = c.f_nsn[f]; h->nsw[f] = c.f_nsw[f]; h->nsi[f] = c.f_nsi[f];
     h->rhead[f] = c.f_rhead[f]; h->retn[f] = c.f_retn[f];
     h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
+    h->warr[f] = c.f_warr[f]; h->hn[f] = c.f_hn[f];
+    h->hist[3 * f] = c.f_hist[3 * f]; h->hist[3 * f + 1] = c.f_hist[3 * f + 1];
+    h->hist[3 * f + 2] = c.f_hist[3 * f + 2];
     h->maxq[f] = c.fs[f].max_queue;
     h->ringoff[f] = c.f_ringoff[f];
     h->slo[f] = c.fs[f].slo_ms;
@@ -125,11 +131,12 @@ __device__ bool hot_load(Ctx& c, H* h) {
   for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.f_loff[f];
   for (int g = c.lane; g < c.G; g += 32) {
     h->sr[g] = c.n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0;
+    h->nplaced[g] = c.n_nplaced[g]; h->fp[g] = c.n_fp[g];
   }
   for (int g = c.lane; g <= c.G; g += 32) h->seg[g] = c.n_seg[g];
   for (int f = c.lane; f < c.F; f += 32) h->coff[f] = c.fs[f].count_off;
   if (c.lane == 0) {
-    h->n = n; h->grants = 0;
+    h->n = n;
     h->counts = c.counts; h->f_ret = c.f_ret; h->f_ring = c.f_ring;
     h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
     h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
@@ -163,12 +170,11 @@ __device__ void hot_store(Ctx& c, H* h) {
     c.f_fw[f] = h->fw[f]; c.f_fi[f] = h->fi[f]; c.f_fn[f] = h->fcnt[f];
     c.f_nsn[f] = h->nsn[f]; c.f_nsw[f] = h->nsw[f]; c.f_nsi[f] = h->nsi[f];
     c.f_rhead[f] = h->rhead[f]; c.f_retn[f] = h->retn[f];
-    c.f_wcomp[f] += h->wcomp[f]; c.f_wviol[f] += h->wviol[f]; c.f_wdrop[f] += h->wdrop[f];
+    c.f_hn[f] = h->hn[f];
+    c.f_hist[3 * f] = h->hist[3 * f]; c.f_hist[3 * f + 1] = h->hist[3 * f + 1];
+    c.f_hist[3 * f + 2] = h->hist[3 * f + 2];
   }
-  for (int g = c.lane; g < c.G; g += 32) {
-    c.n_sr[g] = h->sr[g]; c.n_cov[g] = h->cov[g]; c.n_occ[g] = h->occ[g];
-  }
-  if (c.lane == 0) c.sh->grants += h->grants;
+  for (int g = c.lane; g < c.G; g += 32) c.n_sr[g] = h->sr[g];
   __syncwarp();
 }
 
@@ -401,8 +407,9 @@ __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start,
   h->flags[i] = fl;
 }
 
+// returns the token grants of this step (same value in every lane)
 template <class H>
-__device__ void hot_step(H* h, int lane, int w, int s) {
+__device__ int hot_step(H* h, int lane, int w, int s) {
   const double t0 = (double)w * h->ws + (double)s * h->qs;
   const int n = h->n;
   const int F = h->F, G = h->G;
@@ -525,7 +532,6 @@ __device__ void hot_step(H* h, int lane, int w, int s) {
     }
   }
   grants = warp_sum_i(grants);
-  if (lane == 0) h->grants += grants;
   // serve (sim_engine.py:514-520), pod-parallel.  Granted pods in (function,
   // node, pod_id) order; a dry run counts each pod's request starts, a
   // segmented scan per function turns them into FIFO positions, and a replay
@@ -615,23 +621,41 @@ __device__ void hot_step(H* h, int lane, int w, int s) {
     h->wviol[f] += h->fviol[f];
   }
   __syncwarp();
+  return grants;
 }
 
 template <class H>
-__device__ __noinline__ void hot_steps(H* h, int lane, int w) {
+__device__ __noinline__ long long hot_steps(H* h, int lane, int w) {
   const int T = h->T;
+  long long grants = 0;
   #pragma unroll 1
-  for (int s = 0; s < T; s++) hot_step(h, lane, w, s);
+  for (int s = 0; s < T; s++) grants += hot_step(h, lane, w, s);
   hot_complete(h, lane);
   __syncwarp();
+  return grants;
 }
 
+// Window start when registration did not change (no epoch, nobody warmed
+// up): reset_window + _generate_arrivals directly on the shared-memory set.
 template <class H>
-__device__ bool hot_window(Ctx& c, H* h, int w) {
-  if (!hot_load(c, h)) return false;
-  hot_steps(h, c.lane, w);
-  hot_store(c, h);
-  return true;
+__device__ void hot_begin_light(H* h, int lane, int w) {
+#pragma unroll 1
+  for (int i = lane; i < h->n; i += 32) h->qused[i] = 0.0;
+#pragma unroll 1
+  for (int f = lane; f < h->F; f += 32) {
+    const int n = h->count(f, w);
+    h->warr[f] = n;
+    if (n > 0) {
+      if (h->fcnt[f] == 0) {
+        h->fw[f] = w; h->fi[f] = 0; h->fwn[f] = n;
+        h->farr[f] = h->arrival_n(w, 0, n);
+      }
+      h->fcnt[f] += n;
+    }
+  }
+#pragma unroll 1
+  for (int g = lane; g < h->G; g += 32) { h->cov[g] = 0.0; h->occ[g] = 0.0; }
+  __syncwarp();
 }
 
 }  // namespace gs

@@ -62,7 +62,7 @@ __device__ void init_run(Ctx& c) {
     s->n_reg = 0; s->free_top = c.P; s->win_failures = 0; s->n_batch = 0;
     s->err = 0; s->err_detail = 0; s->err_a0 = 0; s->err_a1 = 0; s->n_list = 0;
     s->grants = 0; s->decisions = 0; s->attempts = 0; s->frag = 0.0;
-    s->pod_steps = 0; s->rect_scans = 0;
+    s->pod_steps = 0; s->rect_scans = 0; s->min_free = c.P;
   }
   __syncwarp();
 }
@@ -121,6 +121,62 @@ __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PyS
   __syncwarp();
 }
 
+// _close_window (sim_engine.py:554-594) from the shared-memory working set
+template <class H>
+__device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, PySum& su,
+                          PySum& so, int& peak, int& fail_total) {
+  const gs_scenario_t& sc = *c.sc;
+  for (int f = c.lane; f < c.F; f += 32) {
+    const int hn = h->hn[f];
+    h->hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
+    h->hn[f] = hn + 1;
+    const int depth = h->qlen[f] + h->fcnt[f];              // len(queue) + len(future)
+    if (out.fn_rows) {
+      gs_fn_row_t r;
+      r.arrivals = h->warr[f]; r.completions = h->wcomp[f]; r.slo_violations = h->wviol[f];
+      r.dropped = h->wdrop[f]; r.queue_depth = depth;
+      out.fn_rows[sc.fn_row_off + (long long)w * c.F + f] = r;
+    }
+    acc.arrivals += h->warr[f]; acc.completions += h->wcomp[f];
+    acc.violations += h->wviol[f]; acc.dropped += h->wdrop[f];
+    if (w == c.W - 1) acc.final_depth += depth;
+    h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
+  }
+  int in_use = 0;
+  for (int g = c.lane; g < c.G; g += 32) {
+    gs_gpu_row_t r;
+    r.present = h->nplaced[g] > 0 ? 1 : 0;
+    r.pad = 0;
+    const double cov = h->cov[g], occ = h->occ[g];
+    r.utilization = r.present ? (cov < 1.0 ? cov : 1.0) : 0.0;
+    r.sm_occupancy = r.present ? (occ < 1.0 ? occ : 1.0) : 0.0;
+    r.memory_mb = r.present ? h->fp[g] : 0.0;
+    if (out.gpu_rows) out.gpu_rows[sc.gpu_row_off + (long long)w * c.G + g] = r;
+    in_use += r.present;
+  }
+  in_use = warp_sum_i(in_use);
+  __syncwarp();
+  if (c.lane == 0) {
+    for (int g = 0; g < c.G; g++) {           // summary sums in CSV row order
+      if (h->nplaced[g] <= 0) continue;
+      const double cov = h->cov[g], occ = h->occ[g];
+      su.add(cov < 1.0 ? cov : 1.0);
+      so.add(occ < 1.0 ? occ : 1.0);
+    }
+    if (out.glob_rows) {
+      gs_glob_row_t r;
+      r.gpus_in_use = in_use;
+      r.placement_failures = c.sh->win_failures;
+      r.fragmentation_index = c.sh->frag;
+      out.glob_rows[sc.glob_row_off + w] = r;
+    }
+    peak = in_use > peak ? in_use : peak;
+    fail_total += c.sh->win_failures;
+    c.sh->win_failures = 0;
+  }
+  __syncwarp();
+}
+
 template <class H> __host__ __device__ constexpr int class_id() {
   if constexpr (std::is_same<H, HotS>::value) return 1;
   else if constexpr (std::is_same<H, HotM>::value) return 2;
@@ -153,21 +209,44 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, int run, H* h) {
   int peak = 0, fail_total = 0;
   if (!failed(c)) place_batch(c);
   if (!failed(c)) refresh_frag(c);
+  bool hot_valid = false;
+  long long pod_steps = 0, hot_grants = 0;   // hot-path counters kept in registers
   for (int w = 0; w < c.W && !failed(c); w++) {
-    if (w > 0 && w % c.sc->epoch_windows == 0) {
-      run_epoch(c, w);
-      if (failed(c)) break;
-    }
-    window_begin(c, w);
+    const bool epoch = w > 0 && w % c.sc->epoch_windows == 0;
     if constexpr (std::is_void<H>::value) {     // XL: working set stays in the HBM arena
+      if (epoch) {
+        run_epoch(c, w);
+        if (failed(c)) break;
+      }
+      window_begin(c, w);
       for (int g = c.lane; g < c.G; g += 32) { c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; }
       __syncwarp();
       for (int s = 0; s < c.T; s++) run_step(c, w, s);
       complete_tokens(c);
+      window_close(c, w, out, acc, su, so, peak, fail_total);
     } else {
-      if (!hot_window(c, h, w)) break;
+      // Registration changes only at epochs and when a placed pod warms up;
+      // otherwise the shared-memory working set carries over to the next window.
+      const bool rebuild = !hot_valid || epoch || w >= c.sh->next_warm;
+      if (rebuild) {
+        if (hot_valid) hot_store(c, h);
+        if (epoch) {
+          run_epoch(c, w);
+          if (failed(c)) break;
+        }
+        window_begin(c, w);
+        if (!hot_load(c, h)) break;
+        hot_valid = true;
+      } else {
+        hot_begin_light(h, c.lane, w);
+      }
+      pod_steps += (long long)h->n * c.T;
+      hot_grants += hot_steps(h, c.lane, w);
+      hot_close(c, h, w, out, acc, su, so, peak, fail_total);
     }
-    window_close(c, w, out, acc, su, so, peak, fail_total);
+  }
+  if constexpr (!std::is_void<H>::value) {
+    if (hot_valid && !c.sh->err) hot_store(c, h);   // flush the last windows' counters
   }
   // outputs
   gs_status_t st;
@@ -199,11 +278,12 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, int run, H* h) {
     st.arg0 = c.sh->err_a0; st.arg1 = c.sh->err_a1;
     st.n_placements = nplaced;
     st.hot_class = class_id<H>();
-    st.token_grants = c.sh->grants;
+    st.token_grants = c.sh->grants + hot_grants;
     st.scale_decisions = c.sh->decisions;
     st.placement_attempts = c.sh->attempts;
-    st.pod_steps = c.sh->pod_steps;
+    st.pod_steps = std::is_void<H>::value ? c.sh->pod_steps : pod_steps;
     st.rect_scans = c.sh->rect_scans;
+    st.peak_pods = c.P - c.sh->min_free;
     out.status[run] = st;
     if (out.summary) {
       gs_summary_t sm;

@@ -114,8 +114,9 @@ struct WarpShared {
   int n_reg, free_top, win_failures, n_batch;
   int err, err_detail, err_a0, err_a1;
   int n_list;
-  int pad;
+  int next_warm;          // earliest warm_at among placed, unregistered pods
   long long grants, decisions, attempts, pod_steps, rect_scans;
+  int min_free;
   double frag;
 };
 
@@ -538,6 +539,7 @@ __device__ int make_pod(Ctx& c, int f, int k, int has_qreq, double qreq, int war
     return -1;
   }
   int slot = c.s_free[--c.sh->free_top];
+  if (c.sh->free_top < c.sh->min_free) c.sh->min_free = c.sh->free_top;
   int ctr = c.f_pctr[f]++;
   c.p_fn[slot] = f; c.p_pt[slot] = k; c.p_node[slot] = -1; c.p_flags[slot] = PF_ALIVE;
   c.p_warm[slot] = warm; c.p_ctr[slot] = ctr; c.p_x[slot] = 0; c.p_y[slot] = 0;
@@ -831,12 +833,19 @@ __device__ void run_epoch(Ctx& c, int w) {
 // and the per-window pod lists
 // ----------------------------------------------------------------------------
 __device__ void window_begin(Ctx& c, int w) {
+  int next_warm = 0x7fffffff;
   for (int slot = c.lane; slot < c.P; slot += 32) {
     int fl = c.p_flags[slot];
-    if ((fl & PF_PLACED) && !(fl & PF_REG) && c.p_warm[slot] <= w) fl |= PF_REG;
+    if ((fl & PF_PLACED) && !(fl & PF_REG)) {
+      if (c.p_warm[slot] <= w) fl |= PF_REG;
+      else next_warm = min(next_warm, c.p_warm[slot]);
+    }
     if (fl & PF_REG) { c.p_qused[slot] = 0.0; fl &= ~PF_GRANT; }
     c.p_flags[slot] = fl;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) next_warm = min(next_warm, __shfl_xor_sync(FULL, next_warm, o));
+  if (c.lane == 0) c.sh->next_warm = next_warm;
   for (int f = c.lane; f < c.F; f += 32) {
     int n = c.count(f, w);
     c.f_warr[f] = n;

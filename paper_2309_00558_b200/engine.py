@@ -37,6 +37,7 @@ class RunResult:
     summary: object = None          # gs_summary_t record (all-gather payload)
     pod_steps: int = 0              # registered-pod x quantum-step updates
     rect_scans: int = 0             # free rectangles examined by best_match
+    peak_pods: int = 0              # most pods alive at once
 
     @property
     def decisions(self) -> int:
@@ -90,7 +91,8 @@ def decode_run(batch: cc.Batch, r: int, out: dict) -> RunResult:
                     scale_decisions=int(st["scale_decisions"]),
                     placement_attempts=int(st["placement_attempts"]),
                     summary=out["summary"][r].copy(),
-                    pod_steps=int(st["pod_steps"]), rect_scans=int(st["rect_scans"]))
+                    pod_steps=int(st["pod_steps"]), rect_scans=int(st["rect_scans"]),
+                    peak_pods=int(st["peak_pods"]))
     pl = out["placements"][int(s["place_off"]): int(s["place_off"]) + int(st["n_placements"])]
     nodes: dict = {g: {} for g in range(G)}
     for node, func, counter, x, y, w_, h, _ in pl.tolist():

@@ -41,7 +41,7 @@ def diff_results(a, b):
     if a.placements != b.placements:
         return "final placements differ"
     for f in ("token_grants", "scale_decisions", "placement_attempts", "pod_steps",
-              "rect_scans"):
+              "rect_scans", "peak_pods"):
         if getattr(a, f) != getattr(b, f):
             return f"{f} {getattr(a, f)} != {getattr(b, f)}"
     if a.summary.tobytes() != b.summary.tobytes():

@@ -15,6 +15,9 @@ from .errors import BackendUnavailableError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libgshare_b200.so")
+# experiments only: GS_LIB points at an alternative build of the same ABI
+if os.environ.get("GS_LIB"):
+    LIB_PATH = os.environ["GS_LIB"]
 
 _lib = None
 _lock = threading.Lock()

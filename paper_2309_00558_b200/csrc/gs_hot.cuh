@@ -182,7 +182,7 @@ __device__ void hot_store(Ctx& c, H* h) {
 // The step loop reads everything through `h` (shared memory): no Ctx, so the
 // whole window stays in a handful of registers.
 template <class H>
-__device__ __forceinline__ void hot_complete_sm(H* h, int lane) {
+__device__ __noinline__ void hot_complete_sm(H* h, int lane) {
   // sm_running -= sm in token (dispatch) order, with the float-dust clamp;
   // only needed when SM partitions are not integers (else it is exactly 0)
   #pragma unroll 1
@@ -407,6 +407,47 @@ __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start,
   h->flags[i] = fl;
 }
 
+// dispatch for non-integral SM partitions: the sequential head-blocking walk
+// with the float sm_running dust (token_backend.py:169-187); returns this
+// lane's grants
+template <class H>
+__device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
+  const double quantum = h->quantum;
+  const int G = h->G;
+  int grants = 0;
+#pragma unroll 1
+    for (int g = lane; g < G; g += 32) {
+      double sr = h->sr[g];
+      double mx = 0.0;
+      PySum occ;
+      occ.reset();
+      int ng = 0;
+      const int e = h->seg[g + 1];
+#pragma unroll 1
+      for (int j = h->seg[g]; j < e; j++) {
+        const int i = h->order[j];
+        if (h->key[i] == ~0ull) break;          // rest of the node is not requesting
+        const double sm = h->sm[i];
+        if (sm + sr > SM_LIMIT + SM_EPS) break;
+        const double rem = h->qlim[i] - h->qused[i];
+        const double dur = rem < quantum ? rem : quantum;
+        h->dur[i] = dur;
+        h->flags[i] |= PF_GRANT;
+        sr += sm;
+        if (ng == 0 || dur > mx) mx = dur;
+        occ.add(sm * dur);
+        ng++;
+      }
+      h->sr[g] = sr;
+      if (ng) {
+        h->cov[g] += mx;
+        h->occ[g] += occ.value() / 100.0;
+      }
+      grants += ng;
+    }
+  return grants;
+}
+
 // returns the token grants of this step (same value in every lane)
 template <class H>
 __device__ int hot_step(H* h, int lane, int w, int s) {
@@ -499,37 +540,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       }
     }
   } else {
-    // general case: sequential head-blocking walk with the float sm_running
-#pragma unroll 1
-    for (int g = lane; g < G; g += 32) {
-      double sr = h->sr[g];
-      double mx = 0.0;
-      PySum occ;
-      occ.reset();
-      int ng = 0;
-      const int e = h->seg[g + 1];
-#pragma unroll 1
-      for (int j = h->seg[g]; j < e; j++) {
-        const int i = h->order[j];
-        if (h->key[i] == ~0ull) break;          // rest of the node is not requesting
-        const double sm = h->sm[i];
-        if (sm + sr > SM_LIMIT + SM_EPS) break;
-        const double rem = h->qlim[i] - h->qused[i];
-        const double dur = rem < quantum ? rem : quantum;
-        h->dur[i] = dur;
-        h->flags[i] |= PF_GRANT;
-        sr += sm;
-        if (ng == 0 || dur > mx) mx = dur;
-        occ.add(sm * dur);
-        ng++;
-      }
-      h->sr[g] = sr;
-      if (ng) {
-        h->cov[g] += mx;
-        h->occ[g] += occ.value() / 100.0;
-      }
-      grants += ng;
-    }
+    grants = hot_dispatch_float(h, lane);
   }
   grants = warp_sum_i(grants);
   // serve (sim_engine.py:514-520), pod-parallel.  Granted pods in (function,

@@ -310,7 +310,10 @@ struct KArgs {
 };
 
 template <class H>
-__global__ void __launch_bounds__(128, 6)
+#ifndef GS_MIN_BLOCKS
+#define GS_MIN_BLOCKS 6   // 128-thread CTAs per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(128, GS_MIN_BLOCKS)
 gs_sim_kernel(KArgs a) {
   __shared__ WarpShared shs[MAX_WARPS_PER_BLOCK];
   extern __shared__ __align__(16) unsigned char dyn_smem[];

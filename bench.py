@@ -11,9 +11,12 @@ A "step" = one launch of the scenario megakernel over the GPU's whole batch.
 ``value``  = total simulated scenario-seconds / device time of the K timed
              launches (CUDA events on the launching stream, max over ranks),
              inputs already resident in HBM, L2 flushed between launches.
-``e2e``    = same metric through the C ABI one-shot call gs_run_batch with
-             host buffers: H2D of the compiled batch, kernel, D2H of every
-             output row -- timed on the host around the call.
+``e2e``    = same metric through the C ABI with host buffers, every step:
+             H2D of the compiled batch from page-locked memory
+             (gs_session_upload), the kernel, and every output row back in
+             host memory (written in place by the kernel into page-locked
+             buffers) plus the status/summary D2H -- host wall clock, max
+             over ranks.
 ``--impl reference`` times the CPU oracle port (oracle/, a literal C
 restatement of pkg/src/gshare_sim, pinned to the reference by golden
 fixtures) on all host cores on a bounded sample of the same workload.
@@ -155,6 +158,14 @@ def cpu_reference(batch, sample_runs: int, threads: int):
     return sim_seconds(sub) / dt, dt, sub
 
 
+def cpu_sample_size(batch, threads: int, target_s: float) -> int:
+    """Runs of `batch` the oracle finishes in about `target_s` seconds on
+    `threads` host threads (calibrated on a small prefix)."""
+    n0 = min(len(batch), max(2 * threads, 32))
+    _, dt, _ = cpu_reference(batch, n0, threads)
+    return int(min(len(batch), max(n0, n0 * target_s / max(dt, 1e-3))))
+
+
 def fleet_totals(summary):
     from paper_2309_00558_b200.dist import summary_totals
     return summary_totals(summary)
@@ -176,14 +187,58 @@ def load_traffic():
         return None
 
 
+def measure_e2e(args, batch, sess, device, dist, compile_s):
+    """The same metric through the C ABI with host buffers: every step uploads
+    the batch from page-locked host memory (gs_session_upload), runs the kernel,
+    and reads every result back (rows written in place into page-locked host
+    memory by the kernel, status + summary by D2H).  Host wall clock around the
+    steps, max over ranks."""
+    import torch
+    batch.pin()
+    out = batch.alloc_outputs(rows=True, pinned=True)
+    sess.map_host(out)
+
+    def step():
+        sess.upload()
+        sess.run()
+        sess.download_into(out)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    world = dist.get_world_size() if dist is not None else 1
+    out_bytes = sum(v.nbytes for v in out.values() if v is not None)
+    sess.map_host(None)
+    return {"value": sim_seconds(batch) * world * args.steps / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(batch.input_bytes()),
+            "d2h_bytes_per_step": int(out_bytes),
+            "ms_per_step": 1000.0 * dt / args.steps,
+            "api": "C ABI session: gs_session_upload (pinned H2D) + gs_session_run + "
+                   "gs_session_download; rows written in place into pinned host memory",
+            "host_compile_s": round(compile_s, 3)}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or max(2 * threads, 64)
-    batch = build_batch(range(sample), args.windows)
+    # each step is a bounded sample (~8 s of CPU work) of the same workload
+    pool = build_batch(range(args.cpu_sample or 4096), args.windows)
+    sample = args.cpu_sample or cpu_sample_size(pool, threads, 8.0)
+    batch = build_batch(range(sample), args.windows) if sample > len(pool) else pool
     for _ in range(args.warmup):
-        cpu_reference(batch, min(sample, threads), threads)
+        cpu_reference(batch, min(sample, 2 * threads), threads)
     times, vals = [], []
     for _ in range(args.steps):
         v, dt, sub = cpu_reference(batch, sample, threads)
@@ -270,6 +325,9 @@ def main():
         fleet = gdist.all_gather_summaries(summ, args.runs * world,
                                            device=torch.device("cuda", local))
     gathered_runs = len(fleet)
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, batch, sess, local, dist, compile_s)
     sim_s = sim_seconds(batch) * world
     value = sim_s / (total_ms / 1000.0 / args.steps)
     st = out["status"]
@@ -282,21 +340,10 @@ def main():
         bytes_launch = algorithmic_bytes(batch, st, summ)
         achieved = bytes_launch / (total_ms / args.steps / 1000.0) / 1e9
         traffic = load_traffic()
-        e2e = None
-        if not args.no_e2e:
-            t0 = time.perf_counter()
-            res = backend.run_batch(batch, device=local, rows=True)
-            e2e_s = time.perf_counter() - t0
-            out_bytes = sum(v.nbytes for v in res.values() if v is not None)
-            e2e = {"value": sim_seconds(batch) / e2e_s, "unit": UNIT,
-                   "h2d_bytes_per_step": int(batch.input_bytes()),
-                   "d2h_bytes_per_step": int(out_bytes),
-                   "api": "gs_run_batch (C ABI, host buffers)",
-                   "host_compile_s": round(compile_s, 3)}
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
-            sample = args.cpu_sample or min(len(batch), max(2 * threads, 64))
+            sample = args.cpu_sample or cpu_sample_size(batch, threads, 15.0)
             v, dt, _ = cpu_reference(batch, sample, threads)
             cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                    "sample": f"first {sample} of the {len(batch)} C2 runs, {dt:.2f} s wall "

@@ -194,8 +194,21 @@ int gs_run_batch(const gs_batch_t* in, const gs_out_t* out, int device, void* st
 int gs_session_create(const gs_batch_t* in, int device, gs_session_t** sess,
                       char* err, size_t err_len);
 int gs_session_run(gs_session_t* sess, void* stream, char* err, size_t err_len);
+/* Re-upload inputs of the same batch shape (per-step H2D of a resident session;
+ * ordered on `stream` before the next gs_session_run on it). */
+int gs_session_upload(gs_session_t* sess, const gs_batch_t* in, void* stream,
+                      char* err, size_t err_len);
 int gs_session_download(gs_session_t* sess, const gs_out_t* out, void* stream,
                         char* err, size_t err_len);
+/* Zero-copy outputs: row buffers of `host` that are page-locked and mapped
+ * (gs_host_alloc / cudaHostAlloc) are filled by the kernel itself -- each run
+ * copies its rows out when it finishes, overlapping the other runs -- and
+ * gs_session_download skips them.  Other pointers are ignored (copied by
+ * download as usual).  gs_run_batch does this automatically. */
+int gs_session_map_host(gs_session_t* sess, const gs_out_t* host);
+/* Page-locked, device-mapped host memory for batch inputs and outputs. */
+int gs_host_alloc(size_t bytes, void** ptr);
+void gs_host_free(void* ptr);
 /* Device pointers of the session's outputs (for device-side collectives). */
 int gs_session_device_out(gs_session_t* sess, gs_out_t* dev_out);
 /* Kernel launches issued by the last gs_session_run / its device time (ms). */

@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 
 from .abi import make_batch_struct, make_out_struct
 from .errors import BackendUnavailableError
@@ -51,6 +52,14 @@ def lib():
             L.gs_session_destroy.restype = None
             L.gs_set_launch.argtypes = [i, i]
             L.gs_set_launch.restype = i
+            L.gs_session_upload.argtypes = [vp, vp, vp, cp, sz]
+            L.gs_session_upload.restype = i
+            L.gs_session_map_host.argtypes = [vp, vp]
+            L.gs_session_map_host.restype = i
+            L.gs_host_alloc.argtypes = [sz, C.POINTER(vp)]
+            L.gs_host_alloc.restype = i
+            L.gs_host_free.argtypes = [vp]
+            L.gs_host_free.restype = None
             if L.gs_abi_version() != 1:
                 raise BackendUnavailableError("libgshare_b200.so ABI version mismatch")
             _lib = L
@@ -63,10 +72,46 @@ def _check(rc: int, err, what: str):
         raise BackendUnavailableError(f"{what}: {err.value.decode(errors='replace')}")
 
 
-def run_batch(batch, device: int = 0, rows: bool = True, stream=None) -> dict:
-    """One-shot: host arrays -> device -> kernel -> host output arrays."""
+class _HostBlock:
+    """Page-locked, device-mapped host allocation (gs_host_alloc); freed when
+    the last numpy view of it is garbage collected."""
+
+    def __init__(self, nbytes: int):
+        self._lib = lib()
+        self.ptr = C.c_void_p()
+        if self._lib.gs_host_alloc(max(int(nbytes), 1), C.byref(self.ptr)) != 0:
+            raise BackendUnavailableError(f"gs_host_alloc({nbytes}) failed")
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value:
+            self._lib.gs_host_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+def host_empty(n: int, dtype):
+    """Uninitialised numpy array of ``n`` records in pinned, mapped host memory."""
+    import numpy as np
+    dtype = np.dtype(dtype)
+    blk = _HostBlock(max(n, 1) * dtype.itemsize)
+    buf = (C.c_char * blk.nbytes).from_address(blk.ptr.value)
+    # numpy views keep `buf` alive; `buf` keeps the block alive until collected
+    _KEEP[id(buf)] = blk
+    weakref.finalize(buf, _KEEP.pop, id(buf), None)
+    return np.frombuffer(buf, dtype=dtype, count=max(n, 1))
+
+
+_KEEP: dict = {}
+
+
+def run_batch(batch, device: int = 0, rows: bool = True, stream=None, out: dict | None = None) -> dict:
+    """One-shot: host arrays -> device -> kernel -> host output arrays.
+
+    ``out`` may be a preallocated output dict (``batch.alloc_outputs(pinned=True)``
+    to reuse page-locked buffers the kernel writes in place)."""
     L = lib()
-    out = batch.alloc_outputs(rows=rows)
+    if out is None:
+        out = batch.alloc_outputs(rows=rows)
     b = make_batch_struct(batch)
     o = make_out_struct(out)
     err = C.create_string_buffer(512)
@@ -95,6 +140,32 @@ class Session:
         rc = self._lib.gs_session_run(self.handle, stream, err, len(err))
         _check(rc, err, "gs_session_run")
         return self._lib.gs_session_last_kernel_ms(self.handle)
+
+    def upload(self, batch=None, stream=None):
+        """Per-step H2D: copy ``batch`` (same shape; default the session's own,
+        e.g. after ``batch.pin()``) into the session's device inputs."""
+        b = make_batch_struct(batch if batch is not None else self.batch)
+        err = C.create_string_buffer(512)
+        rc = self._lib.gs_session_upload(self.handle, C.byref(b), stream, err, len(err))
+        _check(rc, err, "gs_session_upload")
+
+    def map_host(self, out: dict | None):
+        """Let the kernel write ``out``'s page-locked row arrays in place
+        (``None`` unmaps)."""
+        self._host_out = out
+        if out is None:
+            self._lib.gs_session_map_host(self.handle, None)
+            return
+        self._o = make_out_struct(out)
+        self._lib.gs_session_map_host(self.handle, C.byref(self._o))
+
+    def download_into(self, out: dict, stream=None) -> dict:
+        """D2H of everything the kernel did not already write into ``out``."""
+        o = make_out_struct(out)
+        err = C.create_string_buffer(512)
+        rc = self._lib.gs_session_download(self.handle, C.byref(o), stream, err, len(err))
+        _check(rc, err, "gs_session_download")
+        return out
 
     def launches(self) -> int:
         return self._lib.gs_session_last_launches(self.handle)

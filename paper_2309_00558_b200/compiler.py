@@ -434,15 +434,33 @@ class Batch:
     def __len__(self):
         return len(self.images)
 
-    def alloc_outputs(self, rows: bool = True):
+    def alloc_outputs(self, rows: bool = True, pinned: bool = False):
+        """Output arrays.  ``pinned=True`` places the row arrays in page-locked,
+        device-mapped host memory, which the kernel fills in place (zero-copy,
+        overlapped with the simulation); the contents start uninitialised."""
+        if pinned:
+            from .backend import host_empty as alloc
+        else:
+            def alloc(n, dt):
+                return np.zeros(max(n, 1), dt)
         return {
-            "fn_rows": np.zeros(max(self.n_fn_rows, 1), FN_ROW_DT) if rows else None,
-            "gpu_rows": np.zeros(max(self.n_gpu_rows, 1), GPU_ROW_DT) if rows else None,
-            "glob_rows": np.zeros(max(self.n_glob_rows, 1), GLOB_ROW_DT) if rows else None,
-            "placements": np.zeros(max(self.n_placements, 1), PLACEMENT_DT) if rows else None,
+            "fn_rows": alloc(self.n_fn_rows, FN_ROW_DT) if rows else None,
+            "gpu_rows": alloc(self.n_gpu_rows, GPU_ROW_DT) if rows else None,
+            "glob_rows": alloc(self.n_glob_rows, GLOB_ROW_DT) if rows else None,
+            "placements": alloc(self.n_placements, PLACEMENT_DT) if rows else None,
             "status": np.zeros(len(self), STATUS_DT),
             "summary": np.zeros(len(self), SUMMARY_DT),
         }
+
+    def pin(self) -> "Batch":
+        """Move the input arrays to page-locked host memory (fast H2D)."""
+        from .backend import host_empty
+        for name in ("runs", "funcs", "points", "inits", "counts", "names"):
+            a = getattr(self, name)
+            p = host_empty(len(a), a.dtype)
+            p[:len(a)] = a
+            setattr(self, name, p[:len(a)] if len(a) else p)
+        return self
 
     def input_bytes(self) -> int:
         return sum(a.nbytes for a in (self.runs, self.funcs, self.points, self.inits,

@@ -188,8 +188,36 @@ template <class H> __host__ __device__ constexpr size_t hot_bytes() {
   else return sizeof(H);
 }
 
+// Coalesced 4-byte word copy of one run's output rows from HBM to mapped,
+// page-locked host memory (zero-copy): each warp store is one contiguous
+// 128-byte line on PCIe/C2C, and the copy overlaps the other runs' compute.
+__device__ void copy_words(void* dst, const void* src, size_t bytes, int lane) {
+  const unsigned* s = reinterpret_cast<const unsigned*>(src);
+  unsigned* d = reinterpret_cast<unsigned*>(dst);
+  const size_t n = bytes / 4;
+#pragma unroll 4
+  for (size_t k = lane; k < n; k += 32) d[k] = __ldcs(s + k);
+}
+
+__device__ void copy_out_run(const gs_scenario_t& sc, const gs_out_t& out, const gs_out_t& host,
+                             int nplaced, int lane) {
+  const long long W = sc.windows;
+  if (host.fn_rows && out.fn_rows)
+    copy_words(host.fn_rows + sc.fn_row_off, out.fn_rows + sc.fn_row_off,
+               sizeof(gs_fn_row_t) * (size_t)(W * sc.n_funcs), lane);
+  if (host.gpu_rows && out.gpu_rows)
+    copy_words(host.gpu_rows + sc.gpu_row_off, out.gpu_rows + sc.gpu_row_off,
+               sizeof(gs_gpu_row_t) * (size_t)(W * sc.n_nodes), lane);
+  if (host.glob_rows && out.glob_rows)
+    copy_words(host.glob_rows + sc.glob_row_off, out.glob_rows + sc.glob_row_off,
+               sizeof(gs_glob_row_t) * (size_t)W, lane);
+  if (host.placements && out.placements)
+    copy_words(host.placements + sc.place_off, out.placements + sc.place_off,
+               sizeof(gs_placement_t) * (size_t)nplaced, lane);
+}
+
 template <class H>
-__device__ void simulate_run(Ctx& c, const gs_out_t& out, int run, H* h) {
+__device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run, H* h) {
   init_run(c);
   // initial pods: sorted fid order, spec order (sim_engine.py:436-441)
   if (c.lane == 0) {
@@ -297,11 +325,13 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, int run, H* h) {
     }
   }
   __syncwarp();
+  if (!c.sh->err) copy_out_run(*c.sc, out, host, nplaced, c.lane);
 }
 
 struct KArgs {
   gs_batch_t in;              // device pointers
   gs_out_t out;               // device pointers
+  gs_out_t host;              // mapped host mirrors of out's rows (zero-copy), or NULL
   char* arena;
   const long long* ws_off;
   const int* order;           // runs of this size class, longest first
@@ -341,7 +371,7 @@ gs_sim_kernel(KArgs a) {
     c.sh = sh;
     Layout L = run_layout(*c.sc, c.fs);
     ctx_bind(c, a.arena + a.ws_off[run], L);
-    simulate_run<H>(c, a.out, run, hot);
+    simulate_run<H>(c, a.out, a.host, run, hot);
   }
 }
 
@@ -401,6 +431,8 @@ struct gs_session {
   char* arena = nullptr;
   int n_runs = 0;
   int64_t n_fn_rows = 0, n_gpu_rows = 0, n_glob_rows = 0, n_place = 0;
+  gs_out_t host_map{};         // device-visible pointers of mapped host row buffers
+  gs_out_t host_ptr{};         // the same buffers' host addresses (download skips them)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int last_launches = 0;
   double last_ms = 0.0;
@@ -574,6 +606,7 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
     KArgs a;
     a.in = s->dev_in;
     a.out = s->dev_out;
+    a.host = s->host_map;
     a.arena = s->arena;
     a.ws_off = s->ws_off;
     a.order = s->order + lo;
@@ -598,21 +631,54 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
   return GS_OK;
 }
 
+// Re-upload a batch of the same shape (same runs, offsets and sizes) into the
+// session's device buffers: the per-step H2D of a resident session.
+extern "C" int gs_session_upload(gs_session_t* s, const gs_batch_t* in, void* stream_ptr,
+                                 char* err, size_t err_len) {
+  if (!s || !in) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
+  const gs_batch_t& d = s->dev_in;
+  if (in->n_runs != d.n_runs || in->n_funcs != d.n_funcs || in->n_points != d.n_points ||
+      in->n_inits != d.n_inits || in->n_counts != d.n_counts || in->n_names != d.n_names ||
+      in->n_fn_rows != d.n_fn_rows || in->n_gpu_rows != d.n_gpu_rows ||
+      in->n_glob_rows != d.n_glob_rows || in->n_placements != d.n_placements) {
+    put_err(err, err_len, "gs_session_upload: batch shape differs from the session's");
+    return GS_ERR_ARG;
+  }
+  CK(cudaSetDevice(s->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
+  auto up = [&](const void* dst, const void* src, size_t n) -> cudaError_t {
+    if (!src || !n) return cudaSuccess;
+    return cudaMemcpyAsync(const_cast<void*>(dst), src, n, cudaMemcpyHostToDevice, st);
+  };
+  CK(up(d.runs, in->runs, sizeof(gs_scenario_t) * (size_t)in->n_runs));
+  CK(up(d.funcs, in->funcs, sizeof(gs_function_t) * (size_t)in->n_funcs));
+  CK(up(d.points, in->points, sizeof(gs_point_t) * (size_t)in->n_points));
+  CK(up(d.inits, in->inits, sizeof(gs_init_t) * (size_t)in->n_inits));
+  CK(up(d.counts, in->counts, sizeof(int32_t) * (size_t)in->n_counts));
+  CK(up(d.names, in->names, (size_t)in->n_names));
+  return GS_OK;
+}
+
 extern "C" int gs_session_download(gs_session_t* s, const gs_out_t* out, void* stream_ptr,
                                    char* err, size_t err_len) {
   if (!s || !out || !out->status) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
   CK(cudaSetDevice(s->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
-  auto down = [&](void* dst, const void* src, size_t n) -> cudaError_t {
-    if (!dst || !n) return cudaSuccess;
+  auto down = [&](void* dst, const void* src, size_t n, const void* mapped) -> cudaError_t {
+    if (!dst || !n || dst == mapped) return cudaSuccess;   // already written by the kernel
     return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st);
   };
-  CK(down(out->fn_rows, s->dev_out.fn_rows, sizeof(gs_fn_row_t) * (size_t)s->n_fn_rows));
-  CK(down(out->gpu_rows, s->dev_out.gpu_rows, sizeof(gs_gpu_row_t) * (size_t)s->n_gpu_rows));
-  CK(down(out->glob_rows, s->dev_out.glob_rows, sizeof(gs_glob_row_t) * (size_t)s->n_glob_rows));
-  CK(down(out->placements, s->dev_out.placements, sizeof(gs_placement_t) * (size_t)s->n_place));
-  CK(down(out->status, s->dev_out.status, sizeof(gs_status_t) * (size_t)s->n_runs));
-  CK(down(out->summary, s->dev_out.summary, sizeof(gs_summary_t) * (size_t)s->n_runs));
+  const gs_out_t& hp = s->host_ptr;
+  CK(down(out->fn_rows, s->dev_out.fn_rows, sizeof(gs_fn_row_t) * (size_t)s->n_fn_rows,
+          hp.fn_rows));
+  CK(down(out->gpu_rows, s->dev_out.gpu_rows, sizeof(gs_gpu_row_t) * (size_t)s->n_gpu_rows,
+          hp.gpu_rows));
+  CK(down(out->glob_rows, s->dev_out.glob_rows, sizeof(gs_glob_row_t) * (size_t)s->n_glob_rows,
+          hp.glob_rows));
+  CK(down(out->placements, s->dev_out.placements, sizeof(gs_placement_t) * (size_t)s->n_place,
+          hp.placements));
+  CK(down(out->status, s->dev_out.status, sizeof(gs_status_t) * (size_t)s->n_runs, nullptr));
+  CK(down(out->summary, s->dev_out.summary, sizeof(gs_summary_t) * (size_t)s->n_runs, nullptr));
   CK(cudaStreamSynchronize(st));
   int worst = GS_OK;
   for (int r = 0; r < s->n_runs; r++) worst = std::max(worst, (int)out->status[r].code);
@@ -637,11 +703,56 @@ extern "C" void gs_session_destroy(gs_session_t* s) {
   delete s;
 }
 
+// device-visible alias of a page-locked, mapped host pointer (else NULL)
+static void* mapped_alias(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  return at.devicePointer;
+}
+
+extern "C" int gs_session_map_host(gs_session_t* s, const gs_out_t* host) {
+  if (!s) return GS_ERR_ARG;
+  if (cudaSetDevice(s->device) != cudaSuccess) return GS_ERR_CUDA;
+  s->host_map = gs_out_t{};
+  s->host_ptr = gs_out_t{};
+  if (!host) return GS_OK;
+#define GS_MAP(field, T)                                                       \
+  if (void* d_ = mapped_alias(host->field)) {                                  \
+    s->host_map.field = reinterpret_cast<T*>(d_);                              \
+    s->host_ptr.field = host->field;                                           \
+  }
+  GS_MAP(fn_rows, gs_fn_row_t)
+  GS_MAP(gpu_rows, gs_gpu_row_t)
+  GS_MAP(glob_rows, gs_glob_row_t)
+  GS_MAP(placements, gs_placement_t)
+#undef GS_MAP
+  return GS_OK;
+}
+
+extern "C" int gs_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return GS_ERR_ARG;
+  *ptr = nullptr;
+  if (cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable | cudaHostAllocMapped) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return GS_ERR_CUDA;
+  }
+  return GS_OK;
+}
+
+extern "C" void gs_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
 extern "C" int gs_run_batch(const gs_batch_t* in, const gs_out_t* out, int device, void* stream,
                             char* err, size_t err_len) {
   gs_session_t* s = nullptr;
   int rc = gs_session_create(in, device, &s, err, err_len);
   if (rc != GS_OK) return rc;
+  gs_session_map_host(s, out);     // page-locked row buffers are written in place
   rc = gs_session_run(s, stream, err, err_len);
   if (rc == GS_OK) rc = gs_session_download(s, out, stream, err, err_len);
   gs_session_destroy(s);

@@ -30,12 +30,13 @@ template <int PC_, int FC_, int GC_>
 struct Hot {
   static constexpr int PC = PC_, FC = FC_, GC = GC_;
   // registered pods of this window, in (node, pod_id) order
-  double qused[PC], qreq[PC], qlim[PC], sm[PC], busy[PC], crem[PC], carr[PC], invr[PC],
-      dur[PC];
+  // (a granted pod's duration min(quantum, q_lim - q_used) is recomputed where
+  // needed: q_used does not change between dispatch and completion)
+  double qused[PC], qreq[PC], qlim[PC], sm[PC], busy[PC], crem[PC], carr[PC], invr[PC];
   unsigned long long key[PC];
   long long cur[PC];
-  int slot[PC], fnode[PC], flags[PC];
-  short order[PC], flist[PC], rank[PC], gl[PC];
+  int fnode[PC], flags[PC];
+  short order[PC], flist[PC], rank[PC];   // rank doubles as the serve phase's granted list
   // functions
   double farr[FC], slo[FC];
   int qlen[FC], pinned[FC], fw[FC], fi[FC], fcnt[FC], nsn[FC], nsw[FC], nsi[FC];
@@ -43,7 +44,6 @@ struct Hot {
   int fwn[FC], nswn[FC];   // arrival counts of the cursor windows fw / nsw (cached)
   int favail[FC], fcarry[FC], fcomp[FC], fviol[FC];   // parallel-serve scratch
   int warr[FC], hn[FC];
-  double hist[3 * FC];
   int loff[FC + 1];
   int coff[FC];
   // nodes
@@ -61,6 +61,11 @@ struct Hot {
   int n, F, G, T, W, RET, integral;
 
   __device__ __forceinline__ int count(int f, int w) const { return counts[coff[f] + w]; }
+  // token duration of a granted pod: min(quantum, q_limit - q_used) (token_backend.py:178)
+  __device__ __forceinline__ double dur(int i) const {
+    const double rem = qlim[i] - qused[i];
+    return rem < quantum ? rem : quantum;
+  }
   __device__ __forceinline__ double arrival(int f, int w, int i) const {
     // start + i * window_s / n, start = window * window_s (sim_engine.py:463,470)
     return (double)w * ws + ((double)i * ws) / (double)count(f, w);
@@ -97,7 +102,6 @@ __device__ bool hot_load(Ctx& c, H* h) {
   }
   for (int i = c.lane; i < n; i += 32) {
     int s = c.s_rl[i];
-    h->slot[i] = s;
     h->qused[i] = c.p_qused[s];
     h->qreq[i] = c.p_qreq[s];
     h->qlim[i] = c.p_qlim[s];
@@ -106,7 +110,6 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->crem[i] = c.p_crem[s];
     h->carr[i] = c.p_carr[s];
     h->invr[i] = c.p_invr[s];
-    h->dur[i] = 0.0;
     h->cur[i] = pack_id(c.p_cw[s], c.p_ci[s]);
     h->fnode[i] = c.p_fn[s] | (c.p_node[s] << 16);
     h->flags[i] = c.p_flags[s] & PF_CUR;
@@ -119,8 +122,6 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->rhead[f] = c.f_rhead[f]; h->retn[f] = c.f_retn[f];
     h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
     h->warr[f] = c.f_warr[f]; h->hn[f] = c.f_hn[f];
-    h->hist[3 * f] = c.f_hist[3 * f]; h->hist[3 * f + 1] = c.f_hist[3 * f + 1];
-    h->hist[3 * f + 2] = c.f_hist[3 * f + 2];
     h->maxq[f] = c.fs[f].max_queue;
     h->ringoff[f] = c.f_ringoff[f];
     h->slo[f] = c.fs[f].slo_ms;
@@ -156,7 +157,7 @@ template <class H>
 __device__ void hot_store(Ctx& c, H* h) {
   const int n = h->n;
   for (int i = c.lane; i < n; i += 32) {
-    int s = h->slot[i];
+    int s = c.s_rl[i];
     c.p_qused[s] = h->qused[i];
     c.p_busy[s] = h->busy[i];
     c.p_crem[s] = h->crem[i];
@@ -171,8 +172,6 @@ __device__ void hot_store(Ctx& c, H* h) {
     c.f_nsn[f] = h->nsn[f]; c.f_nsw[f] = h->nsw[f]; c.f_nsi[f] = h->nsi[f];
     c.f_rhead[f] = h->rhead[f]; c.f_retn[f] = h->retn[f];
     c.f_hn[f] = h->hn[f];
-    c.f_hist[3 * f] = h->hist[3 * f]; c.f_hist[3 * f + 1] = h->hist[3 * f + 1];
-    c.f_hist[3 * f + 2] = h->hist[3 * f + 2];
   }
   for (int g = c.lane; g < c.G; g += 32) c.n_sr[g] = h->sr[g];
   __syncwarp();
@@ -210,7 +209,7 @@ __device__ __forceinline__ void hot_complete(H* h, int lane) {
   for (int i = lane; i < n; i += 32) {
     const int fl = h->flags[i];
     if (fl & PF_GRANT) {
-      h->qused[i] += h->dur[i];
+      h->qused[i] += h->dur(i);
       h->flags[i] = fl & ~PF_GRANT;
     }
   }
@@ -431,7 +430,6 @@ __device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
         if (sm + sr > SM_LIMIT + SM_EPS) break;
         const double rem = h->qlim[i] - h->qused[i];
         const double dur = rem < quantum ? rem : quantum;
-        h->dur[i] = dur;
         h->flags[i] |= PF_GRANT;
         sr += sm;
         if (ng == 0 || dur > mx) mx = dur;
@@ -465,13 +463,14 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   __syncwarp();
   // complete live tokens + filter_pods + requesting:
   // key = -(q_req - q_used) for requesting pods, ~0 otherwise
+  bool any_req = false;
 #pragma unroll 1
   for (int i = lane; i < n; i += 32) {
     const int f = h->fnode[i] & 0xffff;
     int fl = h->flags[i];
     double qused = h->qused[i];
     if (fl & PF_GRANT) {
-      qused += h->dur[i];
+      qused += h->dur(i);
       h->qused[i] = qused;
       fl &= ~PF_GRANT;
       h->flags[i] = fl;
@@ -479,7 +478,12 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
     h->key[i] = req ? ord_key(-(h->qreq[i] - qused)) : ~0ull;
+    any_req |= req;
   }
+  // No pod requests a token: dispatch grants nothing, so coverage, occupancy,
+  // sm_running and every queue stay as they are (token_backend.py:160-187,
+  // sim_engine.py:514-520 iterate over no tokens).
+  if (!__any_sync(FULL, any_req)) return 0;
   __syncwarp();
   // build_queue order inside each node by rank counting on (key, pod_id)
   // (pod_id order == hot index order within a node).  With integral SM
@@ -515,7 +519,6 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       if (h->key[i] != ~0ull && h->rank[i] < h->cut[g]) {
         const double rem = h->qlim[i] - h->qused[i];
         const double dur = rem < quantum ? rem : quantum;
-        h->dur[i] = dur;
         h->flags[i] |= PF_GRANT;
         atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
         grants++;
@@ -532,7 +535,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       for (int j = h->seg[g]; j < e; j++) {
         const int i = h->order[j];
         if (!(h->flags[i] & PF_GRANT)) break;
-        occ.add(h->sm[i] * h->dur[i]);
+        occ.add(h->sm[i] * h->dur(i));
       }
       if (occ.n) {
         h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
@@ -560,7 +563,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const int i = j < n ? h->flist[j] : 0;
     const bool gr = j < n && (h->flags[i] & PF_GRANT);
     const unsigned bal = __ballot_sync(FULL, gr);
-    if (gr) h->gl[ngl + __popc(bal & ((1u << lane) - 1u))] = (short)i;
+    if (gr) h->rank[ngl + __popc(bal & ((1u << lane) - 1u))] = (short)i;
     ngl += __popc(bal);
   }
   __syncwarp();
@@ -569,9 +572,9 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   for (int k0 = 0; k0 < ngl; k0 += 32) {
     const int k = k0 + lane;
     const bool act = k < ngl;
-    const int i = act ? h->gl[k] : 0;
+    const int i = act ? h->rank[k] : 0;
     const int f = act ? (h->fnode[i] & 0xffff) : -1 - lane;
-    const double t_end = t0 + h->dur[i] * ws;
+    const double t_end = t0 + h->dur(i) * ws;
     const int picks = act ? serve_dry_run(h, i, t0, t_end) : 0;
     int v = picks;
 #pragma unroll

@@ -128,7 +128,7 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
   const gs_scenario_t& sc = *c.sc;
   for (int f = c.lane; f < c.F; f += 32) {
     const int hn = h->hn[f];
-    h->hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
+    c.f_hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
     h->hn[f] = hn + 1;
     const int depth = h->qlen[f] + h->fcnt[f];              // len(queue) + len(future)
     if (out.fn_rows) {

@@ -101,44 +101,44 @@ __device__ bool hot_load(Ctx& c, H* h) {
     return false;
   }
   for (int i = c.lane; i < n; i += 32) {
-    int s = c.s_rl[i];
-    h->qused[i] = c.p_qused[s];
-    h->qreq[i] = c.p_qreq[s];
-    h->qlim[i] = c.p_qlim[s];
-    h->sm[i] = c.p_sm[s];
-    h->busy[i] = c.p_busy[s];
-    h->crem[i] = c.p_crem[s];
-    h->carr[i] = c.p_carr[s];
-    h->invr[i] = c.p_invr[s];
-    h->cur[i] = pack_id(c.p_cw[s], c.p_ci[s]);
-    h->fnode[i] = c.p_fn[s] | (c.p_node[s] << 16);
-    h->flags[i] = c.p_flags[s] & PF_CUR;
+    int s = c.t->s_rl[i];
+    h->qused[i] = c.t->p_qused[s];
+    h->qreq[i] = c.t->p_qreq[s];
+    h->qlim[i] = c.t->p_qlim[s];
+    h->sm[i] = c.t->p_sm[s];
+    h->busy[i] = c.t->p_busy[s];
+    h->crem[i] = c.t->p_crem[s];
+    h->carr[i] = c.t->p_carr[s];
+    h->invr[i] = c.t->p_invr[s];
+    h->cur[i] = pack_id(c.t->p_cw[s], c.t->p_ci[s]);
+    h->fnode[i] = c.t->p_fn[s] | (c.t->p_node[s] << 16);
+    h->flags[i] = c.t->p_flags[s] & PF_CUR;
     h->order[i] = (short)i;
   }
   for (int f = c.lane; f < c.F; f += 32) {
-    h->qlen[f] = c.f_qlen[f]; h->pinned[f] = c.f_pinned[f];
-    h->fw[f] = c.f_fw[f]; h->fi[f] = c.f_fi[f]; h->fcnt[f] = c.f_fn[f];
-    h->nsn[f] = c.f_nsn[f]; h->nsw[f] = c.f_nsw[f]; h->nsi[f] = c.f_nsi[f];
-    h->rhead[f] = c.f_rhead[f]; h->retn[f] = c.f_retn[f];
+    h->qlen[f] = c.t->f_qlen[f]; h->pinned[f] = c.t->f_pinned[f];
+    h->fw[f] = c.t->f_fw[f]; h->fi[f] = c.t->f_fi[f]; h->fcnt[f] = c.t->f_fn[f];
+    h->nsn[f] = c.t->f_nsn[f]; h->nsw[f] = c.t->f_nsw[f]; h->nsi[f] = c.t->f_nsi[f];
+    h->rhead[f] = c.t->f_rhead[f]; h->retn[f] = c.t->f_retn[f];
     h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
-    h->warr[f] = c.f_warr[f]; h->hn[f] = c.f_hn[f];
+    h->warr[f] = c.t->f_warr[f]; h->hn[f] = c.t->f_hn[f];
     h->maxq[f] = c.fs[f].max_queue;
-    h->ringoff[f] = c.f_ringoff[f];
+    h->ringoff[f] = c.t->f_ringoff[f];
     h->slo[f] = c.fs[f].slo_ms;
     h->farr[f] = h->fcnt[f] > 0 ? arrival_time(c, f, h->fw[f], h->fi[f]) : 0.0;
     h->fwn[f] = h->fcnt[f] > 0 ? c.count(f, h->fw[f]) : 1;
     h->nswn[f] = (h->nsn[f] > 0 && c.fs[f].max_queue < 0) ? c.count(f, h->nsw[f]) : 1;
   }
-  for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.f_loff[f];
+  for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.t->f_loff[f];
   for (int g = c.lane; g < c.G; g += 32) {
-    h->sr[g] = c.n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0;
-    h->nplaced[g] = c.n_nplaced[g]; h->fp[g] = c.n_fp[g];
+    h->sr[g] = c.t->n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0;
+    h->nplaced[g] = c.t->n_nplaced[g]; h->fp[g] = c.t->n_fp[g];
   }
-  for (int g = c.lane; g <= c.G; g += 32) h->seg[g] = c.n_seg[g];
+  for (int g = c.lane; g <= c.G; g += 32) h->seg[g] = c.t->n_seg[g];
   for (int f = c.lane; f < c.F; f += 32) h->coff[f] = c.fs[f].count_off;
   if (c.lane == 0) {
     h->n = n;
-    h->counts = c.counts; h->f_ret = c.f_ret; h->f_ring = c.f_ring;
+    h->counts = c.counts; h->f_ret = c.t->f_ret; h->f_ring = c.t->f_ring;
     h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
     h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
     h->integral = c.integral() ? 1 : 0;
@@ -146,9 +146,9 @@ __device__ bool hot_load(Ctx& c, H* h) {
   __syncwarp();
   // s_fl holds arena slots in (node, pod_id) order per function; the hot
   // index of an arena slot is its position in s_rl (slot -> index via s_list).
-  for (int i = c.lane; i < n; i += 32) c.s_list[c.s_rl[i]] = i;
+  for (int i = c.lane; i < n; i += 32) c.t->s_list[c.t->s_rl[i]] = i;
   __syncwarp();
-  for (int j = c.lane; j < n; j += 32) h->flist[j] = (short)c.s_list[c.s_fl[j]];
+  for (int j = c.lane; j < n; j += 32) h->flist[j] = (short)c.t->s_list[c.t->s_fl[j]];
   __syncwarp();
   return true;
 }
@@ -157,23 +157,23 @@ template <class H>
 __device__ void hot_store(Ctx& c, H* h) {
   const int n = h->n;
   for (int i = c.lane; i < n; i += 32) {
-    int s = c.s_rl[i];
-    c.p_qused[s] = h->qused[i];
-    c.p_busy[s] = h->busy[i];
-    c.p_crem[s] = h->crem[i];
-    c.p_carr[s] = h->carr[i];
-    c.p_cw[s] = id_w(h->cur[i]);
-    c.p_ci[s] = id_i(h->cur[i]);
-    c.p_flags[s] = (c.p_flags[s] & ~(PF_CUR | PF_GRANT)) | (h->flags[i] & PF_CUR);
+    int s = c.t->s_rl[i];
+    c.t->p_qused[s] = h->qused[i];
+    c.t->p_busy[s] = h->busy[i];
+    c.t->p_crem[s] = h->crem[i];
+    c.t->p_carr[s] = h->carr[i];
+    c.t->p_cw[s] = id_w(h->cur[i]);
+    c.t->p_ci[s] = id_i(h->cur[i]);
+    c.t->p_flags[s] = (c.t->p_flags[s] & ~(PF_CUR | PF_GRANT)) | (h->flags[i] & PF_CUR);
   }
   for (int f = c.lane; f < c.F; f += 32) {
-    c.f_qlen[f] = h->qlen[f]; c.f_pinned[f] = h->pinned[f];
-    c.f_fw[f] = h->fw[f]; c.f_fi[f] = h->fi[f]; c.f_fn[f] = h->fcnt[f];
-    c.f_nsn[f] = h->nsn[f]; c.f_nsw[f] = h->nsw[f]; c.f_nsi[f] = h->nsi[f];
-    c.f_rhead[f] = h->rhead[f]; c.f_retn[f] = h->retn[f];
-    c.f_hn[f] = h->hn[f];
+    c.t->f_qlen[f] = h->qlen[f]; c.t->f_pinned[f] = h->pinned[f];
+    c.t->f_fw[f] = h->fw[f]; c.t->f_fi[f] = h->fi[f]; c.t->f_fn[f] = h->fcnt[f];
+    c.t->f_nsn[f] = h->nsn[f]; c.t->f_nsw[f] = h->nsw[f]; c.t->f_nsi[f] = h->nsi[f];
+    c.t->f_rhead[f] = h->rhead[f]; c.t->f_retn[f] = h->retn[f];
+    c.t->f_hn[f] = h->hn[f];
   }
-  for (int g = c.lane; g < c.G; g += 32) c.n_sr[g] = h->sr[g];
+  for (int g = c.lane; g < c.G; g += 32) c.t->n_sr[g] = h->sr[g];
   __syncwarp();
 }
 

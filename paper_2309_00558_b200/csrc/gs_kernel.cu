@@ -37,25 +37,25 @@ __host__ __device__ inline Layout run_layout(const gs_scenario_t& sc, const gs_f
 
 __device__ void init_run(Ctx& c) {
   for (int i = c.lane; i < c.P; i += 32) {
-    c.p_flags[i] = 0;
-    c.s_free[i] = c.P - 1 - i;  // slot 0 is allocated first
+    c.t->p_flags[i] = 0;
+    c.t->s_free[i] = c.P - 1 - i;  // slot 0 is allocated first
   }
   for (int f = c.lane; f < c.F; f += 32) {
-    c.f_qlen[f] = 0; c.f_pinned[f] = 0; c.f_fw[f] = 0; c.f_fi[f] = 0; c.f_fn[f] = 0;
-    c.f_nsn[f] = 0; c.f_nsw[f] = 0; c.f_nsi[f] = 0; c.f_rhead[f] = 0; c.f_retn[f] = 0;
-    c.f_pctr[f] = 0; c.f_warr[f] = 0; c.f_wcomp[f] = 0; c.f_wviol[f] = 0; c.f_wdrop[f] = 0;
-    c.f_hn[f] = 0;
+    c.t->f_qlen[f] = 0; c.t->f_pinned[f] = 0; c.t->f_fw[f] = 0; c.t->f_fi[f] = 0; c.t->f_fn[f] = 0;
+    c.t->f_nsn[f] = 0; c.t->f_nsw[f] = 0; c.t->f_nsi[f] = 0; c.t->f_rhead[f] = 0; c.t->f_retn[f] = 0;
+    c.t->f_pctr[f] = 0; c.t->f_warr[f] = 0; c.t->f_wcomp[f] = 0; c.t->f_wviol[f] = 0; c.t->f_wdrop[f] = 0;
+    c.t->f_hn[f] = 0;
   }
   for (int g = c.lane; g < c.G; g += 32) {
-    c.n_sr[g] = 0.0; c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; c.n_fp[g] = 0.0;
-    c.n_nfree[g] = 1; c.n_nres[g] = 0; c.n_nplaced[g] = 0;
-    c.n_rect[g * c.R] = make_int4(0, 0, c.sc->side_x, c.sc->side_y);
+    c.t->n_sr[g] = 0.0; c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; c.t->n_fp[g] = 0.0;
+    c.t->n_nfree[g] = 1; c.t->n_nres[g] = 0; c.t->n_nplaced[g] = 0;
+    c.t->n_rect[g * c.R] = make_int4(0, 0, c.sc->side_x, c.sc->side_y);
   }
-  for (int i = c.lane; i < c.G * c.F; i += 32) c.n_cnt[i] = 0;
+  for (int i = c.lane; i < c.G * c.F; i += 32) c.t->n_cnt[i] = 0;
   if (c.lane == 0) {
     int off = 0;
     for (int f = 0; f < c.F; f++) {
-      c.f_ringoff[f] = off;
+      c.t->f_ringoff[f] = off;
       if (c.fs[f].max_queue > 0) off += c.fs[f].max_queue;
     }
     WarpShared* s = c.sh;
@@ -71,30 +71,30 @@ __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PyS
                              PySum& so, int& peak, int& fail_total) {
   const gs_scenario_t& sc = *c.sc;
   for (int f = c.lane; f < c.F; f += 32) {
-    int hn = c.f_hn[f];
-    c.f_hist[3 * f + hn % 3] = (double)c.f_warr[f] / c.ws;   // history.append(n / W)
-    c.f_hn[f] = hn + 1;
-    int depth = c.f_qlen[f] + c.f_fn[f];                      // len(queue) + len(future)
+    int hn = c.t->f_hn[f];
+    c.t->f_hist[3 * f + hn % 3] = (double)c.t->f_warr[f] / c.ws;   // history.append(n / W)
+    c.t->f_hn[f] = hn + 1;
+    int depth = c.t->f_qlen[f] + c.t->f_fn[f];                      // len(queue) + len(future)
     if (out.fn_rows) {
       gs_fn_row_t r;
-      r.arrivals = c.f_warr[f]; r.completions = c.f_wcomp[f]; r.slo_violations = c.f_wviol[f];
-      r.dropped = c.f_wdrop[f]; r.queue_depth = depth;
+      r.arrivals = c.t->f_warr[f]; r.completions = c.t->f_wcomp[f]; r.slo_violations = c.t->f_wviol[f];
+      r.dropped = c.t->f_wdrop[f]; r.queue_depth = depth;
       out.fn_rows[sc.fn_row_off + (long long)w * c.F + f] = r;
     }
-    acc.arrivals += c.f_warr[f]; acc.completions += c.f_wcomp[f];
-    acc.violations += c.f_wviol[f]; acc.dropped += c.f_wdrop[f];
+    acc.arrivals += c.t->f_warr[f]; acc.completions += c.t->f_wcomp[f];
+    acc.violations += c.t->f_wviol[f]; acc.dropped += c.t->f_wdrop[f];
     if (w == c.W - 1) acc.final_depth += depth;
-    c.f_wcomp[f] = 0; c.f_wviol[f] = 0; c.f_wdrop[f] = 0;
+    c.t->f_wcomp[f] = 0; c.t->f_wviol[f] = 0; c.t->f_wdrop[f] = 0;
   }
   int in_use = 0;
   for (int g = c.lane; g < c.G; g += 32) {
     gs_gpu_row_t r;
-    r.present = c.n_nplaced[g] > 0 ? 1 : 0;
+    r.present = c.t->n_nplaced[g] > 0 ? 1 : 0;
     r.pad = 0;
-    double cov = c.n_cov[g], occ = c.n_occ[g];
+    double cov = c.t->n_cov[g], occ = c.t->n_occ[g];
     r.utilization = r.present ? (cov < 1.0 ? cov : 1.0) : 0.0;
     r.sm_occupancy = r.present ? (occ < 1.0 ? occ : 1.0) : 0.0;
-    r.memory_mb = r.present ? c.n_fp[g] : 0.0;
+    r.memory_mb = r.present ? c.t->n_fp[g] : 0.0;
     if (out.gpu_rows) out.gpu_rows[sc.gpu_row_off + (long long)w * c.G + g] = r;
     in_use += r.present;
   }
@@ -102,8 +102,8 @@ __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PyS
   __syncwarp();
   if (c.lane == 0) {
     for (int g = 0; g < c.G; g++) {           // summary sums in CSV row order
-      if (c.n_nplaced[g] <= 0) continue;
-      double cov = c.n_cov[g], occ = c.n_occ[g];
+      if (c.t->n_nplaced[g] <= 0) continue;
+      double cov = c.t->n_cov[g], occ = c.t->n_occ[g];
       su.add(cov < 1.0 ? cov : 1.0);
       so.add(occ < 1.0 ? occ : 1.0);
     }
@@ -128,7 +128,7 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
   const gs_scenario_t& sc = *c.sc;
   for (int f = c.lane; f < c.F; f += 32) {
     const int hn = h->hn[f];
-    c.f_hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
+    c.t->f_hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
     h->hn[f] = hn + 1;
     const int depth = h->qlen[f] + h->fcnt[f];              // len(queue) + len(future)
     if (out.fn_rows) {
@@ -247,7 +247,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
         if (failed(c)) break;
       }
       window_begin(c, w);
-      for (int g = c.lane; g < c.G; g += 32) { c.n_cov[g] = 0.0; c.n_occ[g] = 0.0; }
+      for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
       __syncwarp();
       for (int s = 0; s < c.T; s++) run_step(c, w, s);
       complete_tokens(c);
@@ -283,13 +283,13 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   if (!c.sh->err) {
     for (int s0 = 0; s0 < c.P; s0 += 32) {
       int slot = s0 + c.lane;
-      bool take = slot < c.P && (c.p_flags[slot] & PF_PLACED);
+      bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED);
       unsigned bal = __ballot_sync(FULL, take);
       if (take && out.placements) {
         int k = nplaced + __popc(bal & ((1u << c.lane) - 1u));
         gs_placement_t p;
-        p.node = c.p_node[slot]; p.func = c.p_fn[slot]; p.counter = c.p_ctr[slot];
-        p.x = c.p_x[slot]; p.y = c.p_y[slot]; p.w = c.p_w[slot]; p.h = c.p_h[slot]; p.pad = 0;
+        p.node = c.t->p_node[slot]; p.func = c.t->p_fn[slot]; p.counter = c.t->p_ctr[slot];
+        p.x = c.t->p_x[slot]; p.y = c.t->p_y[slot]; p.w = c.t->p_w[slot]; p.h = c.t->p_h[slot]; p.pad = 0;
         out.placements[c.sc->place_off + k] = p;
       }
       nplaced += __popc(bal);
@@ -369,6 +369,7 @@ gs_sim_kernel(KArgs a) {
     c.cap_mb = c.sc->capacity_mb;
     c.lane = lane;
     c.sh = sh;
+    c.t = &sh->tab;
     Layout L = run_layout(*c.sc, c.fs);
     ctx_bind(c, a.arena + a.ws_off[run], L);
     simulate_run<H>(c, a.out, a.host, run, hot);

@@ -110,27 +110,10 @@ __device__ __forceinline__ long long warp_max_ll(long long v) {
 // ----------------------------------------------------------------------------
 // per-warp scalars (shared memory) and the run context (registers)
 // ----------------------------------------------------------------------------
-struct WarpShared {
-  int n_reg, free_top, win_failures, n_batch;
-  int err, err_detail, err_a0, err_a1;
-  int n_list;
-  int next_warm;          // earliest warm_at among placed, unregistered pods
-  long long grants, decisions, attempts, pod_steps, rect_scans;
-  int min_free;
-  double frag;
-};
-
-struct Ctx {
-  // inputs
-  const gs_scenario_t* sc;
-  const gs_function_t* fs;
-  const gs_point_t* points;
-  const int32_t* counts;
-  const gs_init_t* inits;
-  int G, F, P, R, RET, W, T, flags, Q;
-  double ws, qs, quantum, cap_mb;
-  int lane;
-  WarpShared* sh;
+// Arena pointers of a run, kept in the warp's shared memory: the window and
+// epoch code reads them with one LDS each instead of holding ~60 pointers in
+// registers (or recomputing the layout chain when they are evicted).
+struct CtxTab {
   // pods
   int *p_fn, *p_pt, *p_node, *p_flags, *p_warm, *p_ctr, *p_x, *p_y, *p_w, *p_h, *p_cw, *p_ci;
   unsigned long long* p_okey;
@@ -153,6 +136,31 @@ struct Ctx {
   int* s_ki;
   int4 *s_carve, *s_rs;
   int2* s_pos;
+};
+
+struct WarpShared {
+  int n_reg, free_top, win_failures, n_batch;
+  int err, err_detail, err_a0, err_a1;
+  int n_list;
+  int next_warm;          // earliest warm_at among placed, unregistered pods
+  long long grants, decisions, attempts, pod_steps, rect_scans;
+  int min_free;
+  double frag;
+  CtxTab tab;
+};
+
+struct Ctx {
+  // inputs
+  const gs_scenario_t* sc;
+  const gs_function_t* fs;
+  const gs_point_t* points;
+  const int32_t* counts;
+  const gs_init_t* inits;
+  int G, F, P, R, RET, W, T, flags, Q;
+  double ws, qs, quantum, cap_mb;
+  int lane;
+  WarpShared* sh;
+  CtxTab* t;         // arena pointers (shared memory)
 
   __device__ const gs_point_t& pt(int f, int k) const { return points[fs[f].point_off + k]; }
   __device__ int count(int f, int w) const { return counts[fs[f].count_off + w]; }
@@ -164,47 +172,51 @@ __device__ __forceinline__ T* carve_ptr(char* base, size_t off) {
   return reinterpret_cast<T*>(base + off);
 }
 
-__device__ void ctx_bind(Ctx& c, char* base, const Layout& L) {
-  c.p_fn = carve_ptr<int>(base, L.p_fn); c.p_pt = carve_ptr<int>(base, L.p_pt);
-  c.p_node = carve_ptr<int>(base, L.p_node); c.p_flags = carve_ptr<int>(base, L.p_flags);
-  c.p_warm = carve_ptr<int>(base, L.p_warm); c.p_ctr = carve_ptr<int>(base, L.p_ctr);
-  c.p_x = carve_ptr<int>(base, L.p_x); c.p_y = carve_ptr<int>(base, L.p_y);
-  c.p_w = carve_ptr<int>(base, L.p_w); c.p_h = carve_ptr<int>(base, L.p_h);
-  c.p_cw = carve_ptr<int>(base, L.p_cw); c.p_ci = carve_ptr<int>(base, L.p_ci);
-  c.p_okey = carve_ptr<unsigned long long>(base, L.p_okey);
-  c.p_sm = carve_ptr<double>(base, L.p_sm); c.p_qreq = carve_ptr<double>(base, L.p_qreq);
-  c.p_qlim = carve_ptr<double>(base, L.p_qlim); c.p_qused = carve_ptr<double>(base, L.p_qused);
-  c.p_busy = carve_ptr<double>(base, L.p_busy); c.p_invr = carve_ptr<double>(base, L.p_invr);
-  c.p_crem = carve_ptr<double>(base, L.p_crem); c.p_carr = carve_ptr<double>(base, L.p_carr);
-  c.p_dur = carve_ptr<double>(base, L.p_dur);
-  c.f_qlen = carve_ptr<int>(base, L.f_qlen); c.f_pinned = carve_ptr<int>(base, L.f_pinned);
-  c.f_fw = carve_ptr<int>(base, L.f_fw); c.f_fi = carve_ptr<int>(base, L.f_fi);
-  c.f_fn = carve_ptr<int>(base, L.f_fn); c.f_nsn = carve_ptr<int>(base, L.f_nsn);
-  c.f_nsw = carve_ptr<int>(base, L.f_nsw); c.f_nsi = carve_ptr<int>(base, L.f_nsi);
-  c.f_rhead = carve_ptr<int>(base, L.f_rhead); c.f_retn = carve_ptr<int>(base, L.f_retn);
-  c.f_pctr = carve_ptr<int>(base, L.f_pctr); c.f_warr = carve_ptr<int>(base, L.f_warr);
-  c.f_wcomp = carve_ptr<int>(base, L.f_wcomp); c.f_wviol = carve_ptr<int>(base, L.f_wviol);
-  c.f_wdrop = carve_ptr<int>(base, L.f_wdrop); c.f_hn = carve_ptr<int>(base, L.f_hn);
-  c.f_ringoff = carve_ptr<int>(base, L.f_ringoff); c.f_loff = carve_ptr<int>(base, L.f_loff);
-  c.f_hist = carve_ptr<double>(base, L.f_hist);
-  c.f_ret = carve_ptr<long long>(base, L.f_ret);
-  c.f_ring = carve_ptr<long long>(base, L.f_ring);
-  c.n_sr = carve_ptr<double>(base, L.n_sr); c.n_cov = carve_ptr<double>(base, L.n_cov);
-  c.n_occ = carve_ptr<double>(base, L.n_occ); c.n_fp = carve_ptr<double>(base, L.n_fp);
-  c.n_nfree = carve_ptr<int>(base, L.n_nfree); c.n_nres = carve_ptr<int>(base, L.n_nres);
-  c.n_nplaced = carve_ptr<int>(base, L.n_nplaced); c.n_seg = carve_ptr<int>(base, L.n_seg);
-  c.n_rect = carve_ptr<int4>(base, L.n_rect);
-  c.n_res = carve_ptr<int2>(base, L.n_res);
-  c.n_cnt = carve_ptr<int>(base, L.n_cnt);
-  c.s_rl = carve_ptr<int>(base, L.s_rl); c.s_fl = carve_ptr<int>(base, L.s_fl);
-  c.s_free = carve_ptr<int>(base, L.s_free); c.s_batch = carve_ptr<int>(base, L.s_batch);
-  c.s_list = carve_ptr<int>(base, L.s_list);
-  c.s_ka = carve_ptr<unsigned long long>(base, L.s_ka);
-  c.s_kd = carve_ptr<unsigned long long>(base, L.s_kd);
-  c.s_ki = carve_ptr<int>(base, L.s_ki);
-  c.s_carve = carve_ptr<int4>(base, L.s_carve);
-  c.s_rs = carve_ptr<int4>(base, L.s_rs);
-  c.s_pos = carve_ptr<int2>(base, L.s_pos);
+__device__ void ctx_bind(Ctx& c, char* base, const Layout& L) {  // lane 0 writes the table
+  CtxTab& t = *c.t;
+  if (c.lane == 0) {
+  t.p_fn = carve_ptr<int>(base, L.p_fn); t.p_pt = carve_ptr<int>(base, L.p_pt);
+  t.p_node = carve_ptr<int>(base, L.p_node); t.p_flags = carve_ptr<int>(base, L.p_flags);
+  t.p_warm = carve_ptr<int>(base, L.p_warm); t.p_ctr = carve_ptr<int>(base, L.p_ctr);
+  t.p_x = carve_ptr<int>(base, L.p_x); t.p_y = carve_ptr<int>(base, L.p_y);
+  t.p_w = carve_ptr<int>(base, L.p_w); t.p_h = carve_ptr<int>(base, L.p_h);
+  t.p_cw = carve_ptr<int>(base, L.p_cw); t.p_ci = carve_ptr<int>(base, L.p_ci);
+  t.p_okey = carve_ptr<unsigned long long>(base, L.p_okey);
+  t.p_sm = carve_ptr<double>(base, L.p_sm); t.p_qreq = carve_ptr<double>(base, L.p_qreq);
+  t.p_qlim = carve_ptr<double>(base, L.p_qlim); t.p_qused = carve_ptr<double>(base, L.p_qused);
+  t.p_busy = carve_ptr<double>(base, L.p_busy); t.p_invr = carve_ptr<double>(base, L.p_invr);
+  t.p_crem = carve_ptr<double>(base, L.p_crem); t.p_carr = carve_ptr<double>(base, L.p_carr);
+  t.p_dur = carve_ptr<double>(base, L.p_dur);
+  t.f_qlen = carve_ptr<int>(base, L.f_qlen); t.f_pinned = carve_ptr<int>(base, L.f_pinned);
+  t.f_fw = carve_ptr<int>(base, L.f_fw); t.f_fi = carve_ptr<int>(base, L.f_fi);
+  t.f_fn = carve_ptr<int>(base, L.f_fn); t.f_nsn = carve_ptr<int>(base, L.f_nsn);
+  t.f_nsw = carve_ptr<int>(base, L.f_nsw); t.f_nsi = carve_ptr<int>(base, L.f_nsi);
+  t.f_rhead = carve_ptr<int>(base, L.f_rhead); t.f_retn = carve_ptr<int>(base, L.f_retn);
+  t.f_pctr = carve_ptr<int>(base, L.f_pctr); t.f_warr = carve_ptr<int>(base, L.f_warr);
+  t.f_wcomp = carve_ptr<int>(base, L.f_wcomp); t.f_wviol = carve_ptr<int>(base, L.f_wviol);
+  t.f_wdrop = carve_ptr<int>(base, L.f_wdrop); t.f_hn = carve_ptr<int>(base, L.f_hn);
+  t.f_ringoff = carve_ptr<int>(base, L.f_ringoff); t.f_loff = carve_ptr<int>(base, L.f_loff);
+  t.f_hist = carve_ptr<double>(base, L.f_hist);
+  t.f_ret = carve_ptr<long long>(base, L.f_ret);
+  t.f_ring = carve_ptr<long long>(base, L.f_ring);
+  t.n_sr = carve_ptr<double>(base, L.n_sr); t.n_cov = carve_ptr<double>(base, L.n_cov);
+  t.n_occ = carve_ptr<double>(base, L.n_occ); t.n_fp = carve_ptr<double>(base, L.n_fp);
+  t.n_nfree = carve_ptr<int>(base, L.n_nfree); t.n_nres = carve_ptr<int>(base, L.n_nres);
+  t.n_nplaced = carve_ptr<int>(base, L.n_nplaced); t.n_seg = carve_ptr<int>(base, L.n_seg);
+  t.n_rect = carve_ptr<int4>(base, L.n_rect);
+  t.n_res = carve_ptr<int2>(base, L.n_res);
+  t.n_cnt = carve_ptr<int>(base, L.n_cnt);
+  t.s_rl = carve_ptr<int>(base, L.s_rl); t.s_fl = carve_ptr<int>(base, L.s_fl);
+  t.s_free = carve_ptr<int>(base, L.s_free); t.s_batch = carve_ptr<int>(base, L.s_batch);
+  t.s_list = carve_ptr<int>(base, L.s_list);
+  t.s_ka = carve_ptr<unsigned long long>(base, L.s_ka);
+  t.s_kd = carve_ptr<unsigned long long>(base, L.s_kd);
+  t.s_ki = carve_ptr<int>(base, L.s_ki);
+  t.s_carve = carve_ptr<int4>(base, L.s_carve);
+  t.s_rs = carve_ptr<int4>(base, L.s_rs);
+  t.s_pos = carve_ptr<int2>(base, L.s_pos);
+  }
+  __syncwarp();
   c.Q = L.Q;
 }
 
@@ -228,9 +240,9 @@ __device__ __forceinline__ bool trip_less(unsigned long long a1, unsigned long l
 }
 
 __device__ void warp_sort(Ctx& c, int n) {
-  unsigned long long* A = c.s_ka;
-  unsigned long long* B = c.s_kd;
-  int* V = c.s_ki;
+  unsigned long long* A = c.t->s_ka;
+  unsigned long long* B = c.t->s_kd;
+  int* V = c.t->s_ki;
   int q = 1;
   while (q < n) q <<= 1;
   if (q < 2) { __syncwarp(); return; }
@@ -301,16 +313,16 @@ __device__ __forceinline__ void advance_id(const Ctx& c, int f, int& w, int& i) 
 // ----------------------------------------------------------------------------
 __device__ void refresh_footprint(Ctx& c, int g) {  // lane-agnostic, single lane
   double total = 0.0;
-  int nres = c.n_nres[g];
+  int nres = c.t->n_nres[g];
   const bool sharing = (c.flags & GS_FLAG_SHARING) != 0;
   for (int i = 0; i < nres; i++) {
-    int2 e = c.n_res[g * c.F + i];
+    int2 e = c.t->n_res[g * c.F + i];
     if (e.y <= 0) continue;
     const gs_function_t& f = c.fs[e.x];
     if (sharing) total += f.mem_server_mb + (double)e.y * f.mem_runtime_mb;
     else total += (double)e.y * f.mem_noshare_mb;
   }
-  c.n_fp[g] = total;
+  c.t->n_fp[g] = total;
 }
 
 __device__ __forceinline__ bool admit(const Ctx& c, int g, int f) {
@@ -318,35 +330,35 @@ __device__ __forceinline__ bool admit(const Ctx& c, int g, int f) {
   double delta;
   if (c.flags & GS_FLAG_SHARING) {
     delta = fs.mem_runtime_mb;
-    if (c.n_cnt[g * c.F + f] <= 0) delta += fs.mem_server_mb;
+    if (c.t->n_cnt[g * c.F + f] <= 0) delta += fs.mem_server_mb;
   } else {
     delta = fs.mem_noshare_mb;
   }
-  return c.n_fp[g] + delta <= c.cap_mb;
+  return c.t->n_fp[g] + delta <= c.cap_mb;
 }
 
 __device__ void mem_add(Ctx& c, int g, int f) {  // single lane
-  int* cnt = &c.n_cnt[g * c.F + f];
-  int2* res = &c.n_res[g * c.F];
+  int* cnt = &c.t->n_cnt[g * c.F + f];
+  int2* res = &c.t->n_res[g * c.F];
   if (*cnt > 0) {
-    int n = c.n_nres[g];
+    int n = c.t->n_nres[g];
     for (int i = 0; i < n; i++) if (res[i].x == f) { res[i].y++; break; }
   } else {
-    res[c.n_nres[g]++] = make_int2(f, 1);
+    res[c.t->n_nres[g]++] = make_int2(f, 1);
   }
   (*cnt)++;
   refresh_footprint(c, g);
 }
 
 __device__ void mem_remove(Ctx& c, int g, int f) {  // single lane
-  int* cnt = &c.n_cnt[g * c.F + f];
-  int2* res = &c.n_res[g * c.F];
-  int n = c.n_nres[g];
+  int* cnt = &c.t->n_cnt[g * c.F + f];
+  int2* res = &c.t->n_res[g * c.F];
+  int n = c.t->n_nres[g];
   for (int i = 0; i < n; i++) {
     if (res[i].x != f) continue;
     if (res[i].y == 1) {            // del resident[fid]: keep the order of the rest
       for (int j = i; j + 1 < n; j++) res[j] = res[j + 1];
-      c.n_nres[g] = n - 1;
+      c.t->n_nres[g] = n - 1;
     } else {
       res[i].y--;
     }
@@ -375,7 +387,7 @@ __device__ __forceinline__ long long r_area(int4 r) { return (long long)r.z * (l
 // when the pruned result would exceed `cap`.
 __device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
   int n = *n_ptr;
-  int4* tmp = c.s_carve;
+  int4* tmp = c.t->s_carve;
   int base = 0;
   for (int s = 0; s < n; s += 32) {
     int j = s + c.lane;
@@ -482,18 +494,18 @@ __device__ BestKey warp_argmin(BestKey k) {
 // best_match (packer.py:169-193): key (r.area - req.area, gpu, y, x), first
 // in (gpu, list) order on full ties.  Returns node (or -1) and the rect.
 __device__ int best_match(Ctx& c, int slot, int4* chosen) {
-  int f = c.p_fn[slot];
-  int rw = c.p_w[slot], rh = c.p_h[slot];
+  int f = c.t->p_fn[slot];
+  int rw = c.t->p_w[slot], rh = c.t->p_h[slot];
   long long rarea = (long long)rw * rh;
   BestKey best;
   best.idx = -1; best.k0 = 0; best.a = best.b = best.d = 0;
   long long scans = 0;
   for (int g = 0; g < c.G; g++) {
     if (!admit(c, g, f)) continue;
-    int nf = c.n_nfree[g];
+    int nf = c.t->n_nfree[g];
     scans += nf;
     for (int j = c.lane; j < nf; j += 32) {
-      int4 r = c.n_rect[g * c.R + j];
+      int4 r = c.t->n_rect[g * c.R + j];
       if (rw <= r.z && rh <= r.w) {
         BestKey k;
         k.k0 = r_area(r) - rarea; k.a = g; k.b = r.y; k.d = r.x; k.idx = g * c.R + j;
@@ -504,7 +516,7 @@ __device__ int best_match(Ctx& c, int slot, int4* chosen) {
   best = warp_argmin(best);
   if (c.lane == 0) c.sh->rect_scans += scans;
   if (best.idx < 0) return -1;
-  *chosen = c.n_rect[best.idx];
+  *chosen = c.t->n_rect[best.idx];
   return best.a;
 }
 
@@ -538,75 +550,75 @@ __device__ int make_pod(Ctx& c, int f, int k, int has_qreq, double qreq, int war
     set_error(c, GS_ERR_CAPACITY, GS_CAP_PODS, c.P, 0);
     return -1;
   }
-  int slot = c.s_free[--c.sh->free_top];
+  int slot = c.t->s_free[--c.sh->free_top];
   if (c.sh->free_top < c.sh->min_free) c.sh->min_free = c.sh->free_top;
-  int ctr = c.f_pctr[f]++;
-  c.p_fn[slot] = f; c.p_pt[slot] = k; c.p_node[slot] = -1; c.p_flags[slot] = PF_ALIVE;
-  c.p_warm[slot] = warm; c.p_ctr[slot] = ctr; c.p_x[slot] = 0; c.p_y[slot] = 0;
-  c.p_w[slot] = p.rect_w; c.p_h[slot] = p.rect_h; c.p_cw[slot] = 0; c.p_ci[slot] = 0;
-  c.p_okey[slot] = (unsigned long long)c.fs[f].id_rank * POW11_10 + digits_key(ctr);
-  c.p_sm[slot] = p.sm_eff;
-  c.p_qlim[slot] = p.quota;
-  c.p_qreq[slot] = has_qreq ? qreq : p.quota;
-  c.p_qused[slot] = 0.0; c.p_busy[slot] = 0.0; c.p_invr[slot] = p.inv_rate;
-  c.p_crem[slot] = 0.0; c.p_carr[slot] = 0.0; c.p_dur[slot] = 0.0;
+  int ctr = c.t->f_pctr[f]++;
+  c.t->p_fn[slot] = f; c.t->p_pt[slot] = k; c.t->p_node[slot] = -1; c.t->p_flags[slot] = PF_ALIVE;
+  c.t->p_warm[slot] = warm; c.t->p_ctr[slot] = ctr; c.t->p_x[slot] = 0; c.t->p_y[slot] = 0;
+  c.t->p_w[slot] = p.rect_w; c.t->p_h[slot] = p.rect_h; c.t->p_cw[slot] = 0; c.t->p_ci[slot] = 0;
+  c.t->p_okey[slot] = (unsigned long long)c.fs[f].id_rank * POW11_10 + digits_key(ctr);
+  c.t->p_sm[slot] = p.sm_eff;
+  c.t->p_qlim[slot] = p.quota;
+  c.t->p_qreq[slot] = has_qreq ? qreq : p.quota;
+  c.t->p_qused[slot] = 0.0; c.t->p_busy[slot] = 0.0; c.t->p_invr[slot] = p.inv_rate;
+  c.t->p_crem[slot] = 0.0; c.t->p_carr[slot] = 0.0; c.t->p_dur[slot] = 0.0;
   return slot;
 }
 
 __device__ void free_slot(Ctx& c, int slot) {  // lane 0
-  c.p_flags[slot] = 0;
-  c.s_free[c.sh->free_top++] = slot;
+  c.t->p_flags[slot] = 0;
+  c.t->s_free[c.sh->free_top++] = slot;
 }
 
 // sorted insert of a returned request id (queue order == id order)
 __device__ void return_request(Ctx& c, int f, long long id) {  // lane 0
-  int n = c.f_retn[f];
+  int n = c.t->f_retn[f];
   if (n >= c.RET) { set_error(c, GS_ERR_CAPACITY, GS_CAP_RETURNED, f, 0); return; }
-  long long* r = &c.f_ret[(size_t)f * c.RET];
+  long long* r = &c.t->f_ret[(size_t)f * c.RET];
   int i = n;
   while (i > 0 && r[i - 1] > id) { r[i] = r[i - 1]; i--; }
   r[i] = id;
-  c.f_retn[f] = n + 1;
+  c.t->f_retn[f] = n + 1;
 }
 
 // _remove_pod: sim_engine.py:377-392 (lane 0)
 __device__ void remove_pod(Ctx& c, int slot) {
-  int fl = c.p_flags[slot];
+  int fl = c.t->p_flags[slot];
   if (fl & PF_RETRY) { free_slot(c, slot); return; }
-  int f = c.p_fn[slot];
+  int f = c.t->p_fn[slot];
   if (fl & PF_CUR) {  // in-flight request restarts from scratch on another pod
-    return_request(c, f, pack_id(c.p_cw[slot], c.p_ci[slot]));
-    c.f_pinned[f]--;
+    return_request(c, f, pack_id(c.t->p_cw[slot], c.t->p_ci[slot]));
+    c.t->f_pinned[f]--;
   }
-  int g = c.p_node[slot];
-  int n = c.n_nfree[g];
+  int g = c.t->p_node[slot];
+  int n = c.t->n_nfree[g];
   if (n >= c.R) { set_error(c, GS_ERR_CAPACITY, GS_CAP_RECTS, g, 0); return; }
-  c.n_rect[g * c.R + n] = make_int4(c.p_x[slot], c.p_y[slot], c.p_w[slot], c.p_h[slot]);
-  c.n_nfree[g] = n + 1;
+  c.t->n_rect[g * c.R + n] = make_int4(c.t->p_x[slot], c.t->p_y[slot], c.t->p_w[slot], c.t->p_h[slot]);
+  c.t->n_nfree[g] = n + 1;
   mem_remove(c, g, f);
-  c.n_nplaced[g]--;
+  c.t->n_nplaced[g]--;
   free_slot(c, slot);
 }
 
 // place() (packer.py:245-261) after best_match chose (g, rect)
 __device__ bool place_pod(Ctx& c, int slot, int g, int4 chosen) {
-  int4 placed = make_int4(chosen.x, chosen.y, c.p_w[slot], c.p_h[slot]);
-  int n = c.n_nfree[g];
+  int4 placed = make_int4(chosen.x, chosen.y, c.t->p_w[slot], c.t->p_h[slot]);
+  int n = c.t->n_nfree[g];
   int nn = n;
-  bool ok = carve(c, &c.n_rect[g * c.R], &nn, placed, c.R);
+  bool ok = carve(c, &c.t->n_rect[g * c.R], &nn, placed, c.R);
   if (!ok) {
     if (c.lane == 0) set_error(c, GS_ERR_CAPACITY, GS_CAP_RECTS, g, 0);
     __syncwarp();
     return false;
   }
   if (c.lane == 0) {
-    c.n_nfree[g] = nn;
-    mem_add(c, g, c.p_fn[slot]);
-    c.n_nplaced[g]++;
-    c.p_node[slot] = g;
-    c.p_x[slot] = chosen.x;
-    c.p_y[slot] = chosen.y;
-    c.p_flags[slot] = (c.p_flags[slot] | PF_PLACED) & ~PF_RETRY;
+    c.t->n_nfree[g] = nn;
+    mem_add(c, g, c.t->p_fn[slot]);
+    c.t->n_nplaced[g]++;
+    c.t->p_node[slot] = g;
+    c.t->p_x[slot] = chosen.x;
+    c.t->p_y[slot] = chosen.y;
+    c.t->p_flags[slot] = (c.t->p_flags[slot] | PF_PLACED) & ~PF_RETRY;
   }
   __syncwarp();
   return true;
@@ -618,21 +630,21 @@ __device__ void place_batch(Ctx& c) {
   int nb = 0;
   for (int s = 0; s < c.P; s += 32) {
     int slot = s + c.lane;
-    bool take = slot < c.P && (c.p_flags[slot] & (PF_ALIVE | PF_PLACED)) == PF_ALIVE;
+    bool take = slot < c.P && (c.t->p_flags[slot] & (PF_ALIVE | PF_PLACED)) == PF_ALIVE;
     unsigned bal = __ballot_sync(FULL, take);
     if (take) {
       int i = nb + __popc(bal & ((1u << c.lane) - 1u));
-      long long area = (long long)c.p_w[slot] * c.p_h[slot];
-      c.s_ka[i] = ~(unsigned long long)area;   // descending area
-      c.s_kd[i] = c.p_okey[slot];
-      c.s_ki[i] = slot;
-      c.p_flags[slot] &= ~PF_RETRY;
+      long long area = (long long)c.t->p_w[slot] * c.t->p_h[slot];
+      c.t->s_ka[i] = ~(unsigned long long)area;   // descending area
+      c.t->s_kd[i] = c.t->p_okey[slot];
+      c.t->s_ki[i] = slot;
+      c.t->p_flags[slot] &= ~PF_RETRY;
     }
     nb += __popc(bal);
   }
   __syncwarp();
   warp_sort(c, nb);
-  for (int i = c.lane; i < nb; i += 32) c.s_batch[i] = c.s_ki[i];
+  for (int i = c.lane; i < nb; i += 32) c.t->s_batch[i] = c.t->s_ki[i];
   __syncwarp();
   // best_match is a pure function of (node state, function, w, h): once a
   // request fails, identical requests fail too until a placement changes the
@@ -640,8 +652,8 @@ __device__ void place_batch(Ctx& c) {
   int memo_f = -1, memo_w = 0, memo_h = 0;
   long long memo_scans = 0;
   for (int i = 0; i < nb; i++) {
-    int slot = c.s_batch[i];
-    int f = c.p_fn[slot], pw = c.p_w[slot], ph = c.p_h[slot];
+    int slot = c.t->s_batch[i];
+    int f = c.t->p_fn[slot], pw = c.t->p_w[slot], ph = c.t->p_h[slot];
     int4 chosen;
     int g;
     if (f == memo_f && pw == memo_w && ph == memo_h) {
@@ -658,7 +670,7 @@ __device__ void place_batch(Ctx& c) {
       memo_f = f; memo_w = pw; memo_h = ph;
       if (c.lane == 0) {
         c.sh->win_failures++;
-        c.p_flags[slot] |= PF_RETRY;
+        c.t->p_flags[slot] |= PF_RETRY;
       }
       __syncwarp();
       continue;
@@ -671,35 +683,35 @@ __device__ void place_batch(Ctx& c) {
 
 // restructure: packer.py:290-320
 __device__ void restructure(Ctx& c, int g) {
-  if (c.n_nfree[g] <= c.sc->restructure_threshold) return;
+  if (c.t->n_nfree[g] <= c.sc->restructure_threshold) return;
   int np = 0;
   for (int s = 0; s < c.P; s += 32) {
     int slot = s + c.lane;
-    bool take = slot < c.P && (c.p_flags[slot] & PF_PLACED) && c.p_node[slot] == g;
+    bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED) && c.t->p_node[slot] == g;
     unsigned bal = __ballot_sync(FULL, take);
     if (take) {
       int i = np + __popc(bal & ((1u << c.lane) - 1u));
-      long long area = (long long)c.p_w[slot] * c.p_h[slot];
-      c.s_ka[i] = ~(unsigned long long)area;
-      c.s_kd[i] = c.p_okey[slot];
-      c.s_ki[i] = slot;
+      long long area = (long long)c.t->p_w[slot] * c.t->p_h[slot];
+      c.t->s_ka[i] = ~(unsigned long long)area;
+      c.t->s_kd[i] = c.t->p_okey[slot];
+      c.t->s_ki[i] = slot;
     }
     np += __popc(bal);
   }
   __syncwarp();
   warp_sort(c, np);
-  for (int i = c.lane; i < np; i += 32) c.s_list[i] = c.s_ki[i];
-  int4* fr = c.s_rs;
+  for (int i = c.lane; i < np; i += 32) c.t->s_list[i] = c.t->s_ki[i];
+  int4* fr = c.t->s_rs;
   int* nfr = &c.sh->n_list;
   if (c.lane == 0) { fr[0] = make_int4(0, 0, c.sc->side_x, c.sc->side_y); *nfr = 1; }
   __syncwarp();
   for (int i = 0; i < np; i++) {
-    int slot = c.s_list[i];
-    int w = c.p_w[slot], h = c.p_h[slot];
+    int slot = c.t->s_list[i];
+    int w = c.t->p_w[slot], h = c.t->p_h[slot];
     int j = best_fit_in_list(c, fr, *nfr, w, h);
     if (j < 0) return;   // abort: node unchanged (packer.py:309-313)
     int4 t = fr[j];
-    if (c.lane == 0) c.s_pos[i] = make_int2(t.x, t.y);
+    if (c.lane == 0) c.t->s_pos[i] = make_int2(t.x, t.y);
     __syncwarp();
     int nn = *nfr;
     if (!carve(c, fr, &nn, make_int4(t.x, t.y, w, h), c.R)) {
@@ -711,13 +723,13 @@ __device__ void restructure(Ctx& c, int g) {
     __syncwarp();
   }
   int nn = *nfr;
-  for (int j = c.lane; j < nn; j += 32) c.n_rect[g * c.R + j] = fr[j];
+  for (int j = c.lane; j < nn; j += 32) c.t->n_rect[g * c.R + j] = fr[j];
   for (int i = c.lane; i < np; i += 32) {
-    int slot = c.s_list[i];
-    c.p_x[slot] = c.s_pos[i].x;
-    c.p_y[slot] = c.s_pos[i].y;
+    int slot = c.t->s_list[i];
+    c.t->p_x[slot] = c.t->s_pos[i].x;
+    c.t->p_y[slot] = c.t->s_pos[i].y;
   }
-  if (c.lane == 0) c.n_nfree[g] = nn;
+  if (c.lane == 0) c.t->n_nfree[g] = nn;
   __syncwarp();
 }
 
@@ -725,9 +737,9 @@ __device__ void restructure(Ctx& c, int g) {
 __device__ void refresh_frag(Ctx& c) {
   long long total = 0, largest = -1;
   for (int g = 0; g < c.G; g++) {
-    int nf = c.n_nfree[g];
+    int nf = c.t->n_nfree[g];
     for (int j = c.lane; j < nf; j += 32) {
-      long long a = r_area(c.n_rect[g * c.R + j]);
+      long long a = r_area(c.t->n_rect[g * c.R + j]);
       total += a;
       largest = a > largest ? a : largest;
     }
@@ -749,21 +761,21 @@ __device__ void run_epoch(Ctx& c, int w) {
     int n = 0;
     for (int s = 0; s < c.P; s += 32) {
       int slot = s + c.lane;
-      bool take = slot < c.P && (c.p_flags[slot] & PF_ALIVE) && c.p_fn[slot] == f;
+      bool take = slot < c.P && (c.t->p_flags[slot] & PF_ALIVE) && c.t->p_fn[slot] == f;
       unsigned bal = __ballot_sync(FULL, take);
       if (take) {
         int i = n + __popc(bal & ((1u << c.lane) - 1u));
-        c.s_ka[i] = ord_key(c.pt(f, c.p_pt[slot]).rpr);
-        c.s_kd[i] = c.p_okey[slot];
-        c.s_ki[i] = slot;
+        c.t->s_ka[i] = ord_key(c.pt(f, c.t->p_pt[slot]).rpr);
+        c.t->s_kd[i] = c.t->p_okey[slot];
+        c.t->s_ki[i] = slot;
       }
       n += __popc(bal);
     }
     __syncwarp();
     warp_sort(c, n);
     if (c.lane == 0) {
-      int hn = c.f_hn[f];
-      const double* h = &c.f_hist[3 * f];
+      int hn = c.t->f_hn[f];
+      const double* h = &c.t->f_hist[3 * f];
       double pred = h[(hn - 1) % 3];          // max(history[-3:])
       for (int b = 2; b <= 3 && b <= hn; b++) {
         double v = h[(hn - b) % 3];
@@ -771,7 +783,7 @@ __device__ void run_epoch(Ctx& c, int w) {
       }
       PySum sup;
       sup.reset();
-      for (int i = 0; i < n; i++) sup.add(c.pt(f, c.p_pt[c.s_ki[i]]).thr);
+      for (int i = 0; i < n; i++) sup.add(c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr);
       double gap = pred - sup.value();        // rps_gap
       if (gap > 0) {                          // scale_up: autoscaler.py:103-131
         const gs_function_t& fs = c.fs[f];
@@ -808,11 +820,11 @@ __device__ void run_epoch(Ctx& c, int w) {
       } else if (gap < 0) {                   // scale_down: autoscaler.py:134-149
         double delta = gap;
         for (int i = 0; i < n && delta < 0; i++) {
-          double t = c.pt(f, c.p_pt[c.s_ki[i]]).thr;
+          double t = c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr;
           if (delta + t > 0) break;
           delta += t;
           c.sh->decisions++;
-          remove_pod(c, c.s_ki[i]);
+          remove_pod(c, c.t->s_ki[i]);
           if (c.sh->err) break;
         }
       }
@@ -835,23 +847,23 @@ __device__ void run_epoch(Ctx& c, int w) {
 __device__ void window_begin(Ctx& c, int w) {
   int next_warm = 0x7fffffff;
   for (int slot = c.lane; slot < c.P; slot += 32) {
-    int fl = c.p_flags[slot];
+    int fl = c.t->p_flags[slot];
     if ((fl & PF_PLACED) && !(fl & PF_REG)) {
-      if (c.p_warm[slot] <= w) fl |= PF_REG;
-      else next_warm = min(next_warm, c.p_warm[slot]);
+      if (c.t->p_warm[slot] <= w) fl |= PF_REG;
+      else next_warm = min(next_warm, c.t->p_warm[slot]);
     }
-    if (fl & PF_REG) { c.p_qused[slot] = 0.0; fl &= ~PF_GRANT; }
-    c.p_flags[slot] = fl;
+    if (fl & PF_REG) { c.t->p_qused[slot] = 0.0; fl &= ~PF_GRANT; }
+    c.t->p_flags[slot] = fl;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) next_warm = min(next_warm, __shfl_xor_sync(FULL, next_warm, o));
   if (c.lane == 0) c.sh->next_warm = next_warm;
   for (int f = c.lane; f < c.F; f += 32) {
     int n = c.count(f, w);
-    c.f_warr[f] = n;
+    c.t->f_warr[f] = n;
     if (n > 0) {
-      if (c.f_fn[f] == 0) { c.f_fw[f] = w; c.f_fi[f] = 0; }
-      c.f_fn[f] += n;
+      if (c.t->f_fn[f] == 0) { c.t->f_fw[f] = w; c.t->f_fi[f] = 0; }
+      c.t->f_fn[f] += n;
     }
   }
   __syncwarp();
@@ -859,43 +871,43 @@ __device__ void window_begin(Ctx& c, int w) {
   int nr = 0;
   for (int s = 0; s < c.P; s += 32) {
     int slot = s + c.lane;
-    bool take = slot < c.P && (c.p_flags[slot] & PF_REG);
+    bool take = slot < c.P && (c.t->p_flags[slot] & PF_REG);
     unsigned bal = __ballot_sync(FULL, take);
     if (take) {
       int i = nr + __popc(bal & ((1u << c.lane) - 1u));
-      c.s_ka[i] = (unsigned long long)c.p_node[slot];
-      c.s_kd[i] = c.p_okey[slot];
-      c.s_ki[i] = slot;
+      c.t->s_ka[i] = (unsigned long long)c.t->p_node[slot];
+      c.t->s_kd[i] = c.t->p_okey[slot];
+      c.t->s_ki[i] = slot;
     }
     nr += __popc(bal);
   }
   __syncwarp();
   warp_sort(c, nr);
-  for (int i = c.lane; i < nr; i += 32) c.s_rl[i] = c.s_ki[i];
+  for (int i = c.lane; i < nr; i += 32) c.t->s_rl[i] = c.t->s_ki[i];
   // node segments
   for (int g = c.lane; g <= c.G; g += 32) {
     // lower bound of node g in the sorted keys
     int lo = 0, hi = nr;
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if ((int)c.s_ka[mid] < g) lo = mid + 1; else hi = mid;
+      if ((int)c.t->s_ka[mid] < g) lo = mid + 1; else hi = mid;
     }
-    c.n_seg[g] = lo;
+    c.t->n_seg[g] = lo;
   }
   __syncwarp();
   // per-function lists in (node, pod_id) order: stable counting sort
   if (c.lane == 0) {
     c.sh->n_reg = nr;
     c.sh->pod_steps += (long long)nr * c.T;
-    for (int f = 0; f <= c.F; f++) c.f_loff[f] = 0;
-    for (int i = 0; i < nr; i++) c.f_loff[c.p_fn[c.s_rl[i]] + 1]++;
-    for (int f = 0; f < c.F; f++) c.f_loff[f + 1] += c.f_loff[f];
+    for (int f = 0; f <= c.F; f++) c.t->f_loff[f] = 0;
+    for (int i = 0; i < nr; i++) c.t->f_loff[c.t->p_fn[c.t->s_rl[i]] + 1]++;
+    for (int f = 0; f < c.F; f++) c.t->f_loff[f + 1] += c.t->f_loff[f];
     for (int i = 0; i < nr; i++) {          // loff[f] doubles as the cursor...
-      int slot = c.s_rl[i];
-      c.s_fl[c.f_loff[c.p_fn[slot]]++] = slot;
+      int slot = c.t->s_rl[i];
+      c.t->s_fl[c.t->f_loff[c.t->p_fn[slot]]++] = slot;
     }
-    for (int f = c.F; f > 0; f--) c.f_loff[f] = c.f_loff[f - 1];  // ...then shifts back
-    c.f_loff[0] = 0;
+    for (int f = c.F; f > 0; f--) c.t->f_loff[f] = c.t->f_loff[f - 1];  // ...then shifts back
+    c.t->f_loff[0] = 0;
   }
   __syncwarp();
 }
@@ -908,34 +920,34 @@ __device__ void complete_tokens(Ctx& c) {  // _complete_live_tokens (sim_engine.
   if (!c.integral()) {
     // sm_running -= sm in token order per node, with the float-dust clamp
     for (int g = c.lane; g < c.G; g += 32) {
-      double sr = c.n_sr[g];
-      for (int j = c.n_seg[g]; j < c.n_seg[g + 1]; j++) {
-        int slot = c.s_rl[c.s_ki[j]];
-        if (!(c.p_flags[slot] & PF_GRANT)) break;
-        sr -= c.p_sm[slot];
+      double sr = c.t->n_sr[g];
+      for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) {
+        int slot = c.t->s_rl[c.t->s_ki[j]];
+        if (!(c.t->p_flags[slot] & PF_GRANT)) break;
+        sr -= c.t->p_sm[slot];
         if (sr < 0 && sr > -SM_EPS) sr = 0.0;
       }
-      c.n_sr[g] = sr;
+      c.t->n_sr[g] = sr;
     }
     __syncwarp();
   }
   for (int i = c.lane; i < n; i += 32) {
-    int slot = c.s_rl[i];
-    int fl = c.p_flags[slot];
+    int slot = c.t->s_rl[i];
+    int fl = c.t->p_flags[slot];
     if (fl & PF_GRANT) {
-      c.p_qused[slot] += c.p_dur[slot];
-      c.p_flags[slot] = fl & ~PF_GRANT;
+      c.t->p_qused[slot] += c.t->p_dur[slot];
+      c.t->p_flags[slot] = fl & ~PF_GRANT;
     }
   }
   __syncwarp();
 }
 
 __device__ void admit_arrivals(Ctx& c, int f, double t0) {  // sim_engine.py:472-480
-  int fn = c.f_fn[f];
+  int fn = c.t->f_fn[f];
   if (fn == 0) return;
-  int w = c.f_fw[f], i = c.f_fi[f];
+  int w = c.t->f_fw[f], i = c.t->f_fi[f];
   int limit = c.fs[f].max_queue;
-  int qlen = c.f_qlen[f], nsn = c.f_nsn[f];
+  int qlen = c.t->f_qlen[f], nsn = c.t->f_nsn[f];
   int drop = 0;
   double now = t0 + TIME_EPS;
   while (fn > 0 && arrival_time(c, f, w, i) <= now) {
@@ -945,78 +957,78 @@ __device__ void admit_arrivals(Ctx& c, int f, double t0) {  // sim_engine.py:472
     if (limit >= 0 && qlen >= limit) { drop++; continue; }
     qlen++;
     if (limit < 0) {
-      if (nsn == 0) { c.f_nsw[f] = aw; c.f_nsi[f] = ai; }
+      if (nsn == 0) { c.t->f_nsw[f] = aw; c.t->f_nsi[f] = ai; }
     } else {
       int cap = limit;
-      c.f_ring[c.f_ringoff[f] + (c.f_rhead[f] + nsn) % cap] = pack_id(aw, ai);
+      c.t->f_ring[c.t->f_ringoff[f] + (c.t->f_rhead[f] + nsn) % cap] = pack_id(aw, ai);
     }
     nsn++;
   }
-  c.f_fn[f] = fn; c.f_fw[f] = w; c.f_fi[f] = i;
-  c.f_qlen[f] = qlen; c.f_nsn[f] = nsn;
-  c.f_wdrop[f] += drop;
+  c.t->f_fn[f] = fn; c.t->f_fw[f] = w; c.t->f_fi[f] = i;
+  c.t->f_qlen[f] = qlen; c.t->f_nsn[f] = nsn;
+  c.t->f_wdrop[f] += drop;
 }
 
 // _serve: sim_engine.py:525-552
 __device__ void serve(Ctx& c, int slot, double t_start, double t_end) {
-  int f = c.p_fn[slot];
-  int fl = c.p_flags[slot];
-  double busy = c.p_busy[slot];
+  int f = c.t->p_fn[slot];
+  int fl = c.t->p_flags[slot];
+  double busy = c.t->p_busy[slot];
   double t = busy > t_start ? busy : t_start;
-  if (!(t < t_end - TIME_EPS)) { c.p_busy[slot] = t; return; }
-  double rem = c.p_crem[slot], arr = c.p_carr[slot];
+  if (!(t < t_end - TIME_EPS)) { c.t->p_busy[slot] = t; return; }
+  double rem = c.t->p_crem[slot], arr = c.t->p_carr[slot];
   double slo = c.fs[f].slo_ms;
   int comp = 0, viol = 0;
   while (t < t_end - TIME_EPS) {
     if (!(fl & PF_CUR)) {
       long long id;
-      int retn = c.f_retn[f];
-      int nsn = c.f_nsn[f];
+      int retn = c.t->f_retn[f];
+      int nsn = c.t->f_nsn[f];
       if (retn > 0) {
-        long long* r = &c.f_ret[(size_t)f * c.RET];
+        long long* r = &c.t->f_ret[(size_t)f * c.RET];
         id = r[0];
         for (int k = 1; k < retn; k++) r[k - 1] = r[k];
-        c.f_retn[f] = retn - 1;
+        c.t->f_retn[f] = retn - 1;
       } else if (nsn > 0) {
         int limit = c.fs[f].max_queue;
         if (limit < 0) {
-          int nw = c.f_nsw[f], ni = c.f_nsi[f];
+          int nw = c.t->f_nsw[f], ni = c.t->f_nsi[f];
           id = pack_id(nw, ni);
-          if (nsn > 1) { advance_id(c, f, nw, ni); c.f_nsw[f] = nw; c.f_nsi[f] = ni; }
+          if (nsn > 1) { advance_id(c, f, nw, ni); c.t->f_nsw[f] = nw; c.t->f_nsi[f] = ni; }
         } else {
-          int h = c.f_rhead[f];
-          id = c.f_ring[c.f_ringoff[f] + h];
-          c.f_rhead[f] = (h + 1) % limit;
+          int h = c.t->f_rhead[f];
+          id = c.t->f_ring[c.t->f_ringoff[f] + h];
+          c.t->f_rhead[f] = (h + 1) % limit;
         }
-        c.f_nsn[f] = nsn - 1;
+        c.t->f_nsn[f] = nsn - 1;
       } else {
         break;
       }
-      c.f_pinned[f]++;
+      c.t->f_pinned[f]++;
       fl |= PF_CUR;
-      rem = c.p_invr[slot];
+      rem = c.t->p_invr[slot];
       arr = arrival_time(c, f, id_w(id), id_i(id));
-      c.p_cw[slot] = id_w(id);
-      c.p_ci[slot] = id_i(id);
+      c.t->p_cw[slot] = id_w(id);
+      c.t->p_ci[slot] = id_i(id);
     }
     double left = t_end - t;
     double span = rem < left ? rem : left;
     rem -= span;
     t += span;
     if (rem <= TIME_EPS) {
-      c.f_qlen[f]--;
-      c.f_pinned[f]--;
+      c.t->f_qlen[f]--;
+      c.t->f_pinned[f]--;
       fl &= ~PF_CUR;
       comp++;
       if ((t - arr) * 1000.0 > slo) viol++;
     }
   }
-  c.p_busy[slot] = t;
-  c.p_crem[slot] = rem;
-  c.p_carr[slot] = arr;
-  c.p_flags[slot] = fl;
-  c.f_wcomp[f] += comp;
-  c.f_wviol[f] += viol;
+  c.t->p_busy[slot] = t;
+  c.t->p_crem[slot] = rem;
+  c.t->p_carr[slot] = arr;
+  c.t->p_flags[slot] = fl;
+  c.t->f_wcomp[f] += comp;
+  c.t->f_wviol[f] += viol;
 }
 
 __device__ void run_step(Ctx& c, int w, int s) {
@@ -1027,44 +1039,44 @@ __device__ void run_step(Ctx& c, int w, int s) {
   // filter_pods + requesting + build_queue keys
   const int n = c.sh->n_reg;
   for (int i = c.lane; i < n; i += 32) {
-    int slot = c.s_rl[i];
-    int fl = c.p_flags[slot];
-    double qused = c.p_qused[slot];
-    bool cand = !(c.p_qlim[slot] - qused <= QUOTA_EPS);
-    int f = c.p_fn[slot];
-    bool req = cand && ((fl & PF_CUR) || (c.f_qlen[f] - c.f_pinned[f] > 0));
-    c.s_ka[i] = ((unsigned long long)c.p_node[slot] << 1) | (req ? 0ull : 1ull);
-    c.s_kd[i] = req ? ord_key(-(c.p_qreq[slot] - qused)) : 0ull;
-    c.s_ki[i] = i;
+    int slot = c.t->s_rl[i];
+    int fl = c.t->p_flags[slot];
+    double qused = c.t->p_qused[slot];
+    bool cand = !(c.t->p_qlim[slot] - qused <= QUOTA_EPS);
+    int f = c.t->p_fn[slot];
+    bool req = cand && ((fl & PF_CUR) || (c.t->f_qlen[f] - c.t->f_pinned[f] > 0));
+    c.t->s_ka[i] = ((unsigned long long)c.t->p_node[slot] << 1) | (req ? 0ull : 1ull);
+    c.t->s_kd[i] = req ? ord_key(-(c.t->p_qreq[slot] - qused)) : 0ull;
+    c.t->s_ki[i] = i;
   }
   __syncwarp();
   warp_sort(c, n);
   // dispatch (head-blocking) + coverage/occupancy, one lane per node
   int grants = 0;
   for (int g = c.lane; g < c.G; g += 32) {
-    double sr = c.integral() ? 0.0 : c.n_sr[g];
+    double sr = c.integral() ? 0.0 : c.t->n_sr[g];
     double mx = 0.0;
     PySum occ;
     occ.reset();
     int ng = 0;
-    for (int j = c.n_seg[g]; j < c.n_seg[g + 1]; j++) {
-      if (c.s_ka[j] & 1ull) break;           // rest of the node is not requesting
-      int slot = c.s_rl[c.s_ki[j]];
-      double sm = c.p_sm[slot];
+    for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) {
+      if (c.t->s_ka[j] & 1ull) break;           // rest of the node is not requesting
+      int slot = c.t->s_rl[c.t->s_ki[j]];
+      double sm = c.t->p_sm[slot];
       if (sm + sr > SM_LIMIT + SM_EPS) break;
-      double rem = c.p_qlim[slot] - c.p_qused[slot];
+      double rem = c.t->p_qlim[slot] - c.t->p_qused[slot];
       double dur = rem < c.quantum ? rem : c.quantum;
-      c.p_dur[slot] = dur;
-      c.p_flags[slot] |= PF_GRANT;
+      c.t->p_dur[slot] = dur;
+      c.t->p_flags[slot] |= PF_GRANT;
       sr += sm;
       if (ng == 0 || dur > mx) mx = dur;
       occ.add(sm * dur);
       ng++;
     }
-    if (!c.integral()) c.n_sr[g] = sr;
+    if (!c.integral()) c.t->n_sr[g] = sr;
     if (ng) {
-      c.n_cov[g] += mx;
-      c.n_occ[g] += occ.value() / 100.0;
+      c.t->n_cov[g] += mx;
+      c.t->n_occ[g] += occ.value() / 100.0;
     }
     grants += ng;
   }
@@ -1073,9 +1085,9 @@ __device__ void run_step(Ctx& c, int w, int s) {
   __syncwarp();
   // serve, per function in (node, pod_id) order
   for (int f = c.lane; f < c.F; f += 32) {
-    for (int j = c.f_loff[f]; j < c.f_loff[f + 1]; j++) {
-      int slot = c.s_fl[j];
-      if (c.p_flags[slot] & PF_GRANT) serve(c, slot, t0, t0 + c.p_dur[slot] * c.ws);
+    for (int j = c.t->f_loff[f]; j < c.t->f_loff[f + 1]; j++) {
+      int slot = c.t->s_fl[j];
+      if (c.t->p_flags[slot] & PF_GRANT) serve(c, slot, t0, t0 + c.t->p_dur[slot] * c.ws);
     }
   }
   __syncwarp();

@@ -136,6 +136,7 @@ struct CtxTab {
   int* s_ki;
   int4 *s_carve, *s_rs;
   int2* s_pos;
+  int* s_fcur;
 };
 
 struct WarpShared {
@@ -215,6 +216,7 @@ __device__ void ctx_bind(Ctx& c, char* base, const Layout& L) {  // lane 0 write
   t.s_carve = carve_ptr<int4>(base, L.s_carve);
   t.s_rs = carve_ptr<int4>(base, L.s_rs);
   t.s_pos = carve_ptr<int2>(base, L.s_pos);
+  t.s_fcur = carve_ptr<int>(base, L.s_fcur);
   }
   __syncwarp();
   c.Q = L.Q;
@@ -754,79 +756,175 @@ __device__ void refresh_frag(Ctx& c) {
 // ----------------------------------------------------------------------------
 // epoch: _run_epoch (sim_engine.py:409-430), autoscaler.py:81-160
 // ----------------------------------------------------------------------------
+// register bitonic sort of one (a, b, v) triple per lane, ascending over the
+// first n lanes (n <= 32); lanes >= n must hold (~0, ~0, INT_MAX)
+__device__ __forceinline__ void warp_sort_regs(unsigned long long& a, unsigned long long& b,
+                                               int& v, int n, int lane) {
+  int q = 1;
+  while (q < n) q <<= 1;
+  for (int k = 2; k <= q; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const unsigned long long oa = __shfl_xor_sync(FULL, a, j);
+      const unsigned long long ob = __shfl_xor_sync(FULL, b, j);
+      const int ov = __shfl_xor_sync(FULL, v, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      const bool other_less = trip_less(oa, ob, ov, a, b, v);
+      const bool take = lower == up ? other_less : !other_less && !(oa == a && ob == b && ov == v);
+      if (take) { a = oa; b = ob; v = ov; }
+    }
+  }
+}
+
+// alive pods grouped by function, slot order inside a group:
+// s_list[f_loff[f] .. f_loff[f+1]).  (f_loff is scratch until window_begin.)
+__device__ void group_alive_by_fn(Ctx& c) {
+  int* off = c.t->f_loff;
+  int* cur = c.t->s_fcur;
+  for (int f = c.lane; f <= c.F; f += 32) cur[f] = 0;
+  __syncwarp();
+  for (int s0 = 0; s0 < c.P; s0 += 32) {
+    const int slot = s0 + c.lane;
+    const int fn = (slot < c.P && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
+    const unsigned m = __match_any_sync(FULL, fn);
+    if (fn >= 0 && c.lane == __ffs(m) - 1) atomicAdd(&cur[fn], __popc(m));
+  }
+  __syncwarp();
+  if (c.lane == 0) {                       // exclusive scan (F is small)
+    int acc = 0;
+    for (int f = 0; f < c.F; f++) { off[f] = acc; const int n = cur[f]; cur[f] = acc; acc += n; }
+    off[c.F] = acc;
+  }
+  __syncwarp();
+  for (int s0 = 0; s0 < c.P; s0 += 32) {
+    const int slot = s0 + c.lane;
+    const int fn = (slot < c.P && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
+    const unsigned m = __match_any_sync(FULL, fn);
+    if (fn >= 0) {
+      const int pos = cur[fn] + __popc(m & ((1u << c.lane) - 1u));
+      c.t->s_list[pos] = slot;
+    }
+    __syncwarp();
+    if (fn >= 0 && c.lane == __ffs(m) - 1) cur[fn] += __popc(m);
+    __syncwarp();
+  }
+}
+
+// scale_up's p_ideal (autoscaler.py:120-126): argmin over points with T > r of
+// (T - r, area, sm, quota); points are distinct in (sm, quota), so the
+// reference's first-strict-minimum is the unique lexicographic minimum.
+__device__ int ideal_point(const Ctx& c, int f, double residual) {
+  const gs_function_t& fs = c.fs[f];
+  double k0 = 0, k1 = 0, k2 = 0, k3 = 0;
+  int idx = -1;
+  for (int k = c.lane; k < fs.n_points; k += 32) {
+    const gs_point_t& p = c.pt(f, k);
+    if (!(p.thr > residual)) continue;
+    const double d = p.thr - residual;
+    if (idx < 0 || d < k0 || (d == k0 && (p.area < k1 || (p.area == k1 &&
+        (p.sm < k2 || (p.sm == k2 && p.quota < k3)))))) {
+      k0 = d; k1 = p.area; k2 = p.sm; k3 = p.quota; idx = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double y0 = __shfl_xor_sync(FULL, k0, o), y1 = __shfl_xor_sync(FULL, k1, o);
+    const double y2 = __shfl_xor_sync(FULL, k2, o), y3 = __shfl_xor_sync(FULL, k3, o);
+    const int yi = __shfl_xor_sync(FULL, idx, o);
+    bool take;
+    if (yi < 0) take = false;
+    else if (idx < 0) take = true;
+    else take = y0 < k0 || (y0 == k0 && (y1 < k1 || (y1 == k1 && (y2 < k2 || (y2 == k2 &&
+                (y3 < k3 || (y3 == k3 && yi < idx)))))));
+    if (take) { k0 = y0; k1 = y1; k2 = y2; k3 = y3; idx = yi; }
+  }
+  return idx;
+}
+
+// ----------------------------------------------------------------------------
+// epoch: _run_epoch (sim_engine.py:409-430), autoscaler.py:81-160
+// ----------------------------------------------------------------------------
 __device__ void run_epoch(Ctx& c, int w) {
+  group_alive_by_fn(c);
   for (int f = 0; f < c.F; f++) {
     // running set of f: placed pods + retry pods (sim_engine.py:370-375),
-    // ordered by (efficiency, pod_id) (autoscaler.py:50-51)
-    int n = 0;
-    for (int s = 0; s < c.P; s += 32) {
-      int slot = s + c.lane;
-      bool take = slot < c.P && (c.t->p_flags[slot] & PF_ALIVE) && c.t->p_fn[slot] == f;
-      unsigned bal = __ballot_sync(FULL, take);
-      if (take) {
-        int i = n + __popc(bal & ((1u << c.lane) - 1u));
+    // ordered by (efficiency, pod_id) (autoscaler.py:50-51); T in that order
+    const int start = c.t->f_loff[f];
+    const int n = c.t->f_loff[f + 1] - start;
+    double thr = 0.0;                       // lane i: T of the i-th running pod (n <= 32)
+    PySum sup;
+    sup.reset();
+    if (n <= 32) {
+      unsigned long long a = ~0ull, b = ~0ull;
+      int v = 0x7fffffff;
+      if (c.lane < n) {
+        const int slot = c.t->s_list[start + c.lane];
+        a = ord_key(c.pt(f, c.t->p_pt[slot]).rpr);
+        b = c.t->p_okey[slot];
+        v = slot;
+      }
+      warp_sort_regs(a, b, v, n, c.lane);
+      if (c.lane < n) {
+        thr = c.pt(f, c.t->p_pt[v]).thr;
+        c.t->s_ki[c.lane] = v;
+      }
+      for (int i = 0; i < n; i++) sup.add(__shfl_sync(FULL, thr, i));   // same in every lane
+      __syncwarp();
+    } else {
+      for (int i = c.lane; i < n; i += 32) {
+        const int slot = c.t->s_list[start + i];
         c.t->s_ka[i] = ord_key(c.pt(f, c.t->p_pt[slot]).rpr);
         c.t->s_kd[i] = c.t->p_okey[slot];
         c.t->s_ki[i] = slot;
       }
-      n += __popc(bal);
-    }
-    __syncwarp();
-    warp_sort(c, n);
-    if (c.lane == 0) {
-      int hn = c.t->f_hn[f];
-      const double* h = &c.t->f_hist[3 * f];
-      double pred = h[(hn - 1) % 3];          // max(history[-3:])
-      for (int b = 2; b <= 3 && b <= hn; b++) {
-        double v = h[(hn - b) % 3];
-        if (v > pred) pred = v;
-      }
-      PySum sup;
-      sup.reset();
+      __syncwarp();
+      warp_sort(c, n);
       for (int i = 0; i < n; i++) sup.add(c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr);
-      double gap = pred - sup.value();        // rps_gap
-      if (gap > 0) {                          // scale_up: autoscaler.py:103-131
-        const gs_function_t& fs = c.fs[f];
-        int pe = fs.p_eff;
-        double t_eff = c.pt(f, pe).thr;
-        double nd = floor(gap / t_eff);
-        double residual = gap - nd * t_eff;
-        long long cnt = (long long)nd;
-        int ideal = -1;
-        if (residual > 0) {
-          ideal = pe;
-          bool found = false;
-          double b0 = 0, b1 = 0, b2 = 0, b3 = 0;
-          for (int k = 0; k < fs.n_points; k++) {
-            const gs_point_t& p = c.pt(f, k);
-            if (!(p.thr > residual)) continue;
-            double k0 = p.thr - residual;
-            if (!found || k0 < b0 || (k0 == b0 && (p.area < b1 || (p.area == b1 &&
-                (p.sm < b2 || (p.sm == b2 && p.quota < b3)))))) {
-              found = true; b0 = k0; b1 = p.area; b2 = p.sm; b3 = p.quota; ideal = k;
-            }
-          }
-        }
-        long long total = cnt + (ideal >= 0 ? 1 : 0);
+    }
+    const int hn = c.t->f_hn[f];
+    const double* h = &c.t->f_hist[3 * f];
+    double pred = h[(hn - 1) % 3];            // max(history[-3:])
+    for (int k = 2; k <= 3 && k <= hn; k++) {
+      const double x = h[(hn - k) % 3];
+      if (x > pred) pred = x;
+    }
+    const double gap = pred - sup.value();    // rps_gap
+    if (gap > 0) {                            // scale_up: autoscaler.py:103-131
+      const gs_function_t& fs = c.fs[f];
+      const int pe = fs.p_eff;
+      const double t_eff = c.pt(f, pe).thr;
+      const double nd = floor(gap / t_eff);
+      const double residual = gap - nd * t_eff;
+      const long long cnt = (long long)nd;
+      int ideal = -1;
+      if (residual > 0) {
+        ideal = ideal_point(c, f, residual);
+        if (ideal < 0) ideal = pe;
+      }
+      if (c.lane == 0) {
+        const long long total = cnt + (ideal >= 0 ? 1 : 0);
         c.sh->decisions += total;
         if (total > c.P) {
           set_error(c, GS_ERR_CAPACITY, GS_CAP_PODS, c.P, 1);
         } else {
           for (long long i = 0; i < total; i++) {
-            int k = i < cnt ? pe : ideal;
+            const int k = i < cnt ? pe : ideal;
             if (make_pod(c, f, k, 0, 0.0, w + c.sc->cold_start_windows) < 0) break;
           }
         }
-      } else if (gap < 0) {                   // scale_down: autoscaler.py:134-149
-        double delta = gap;
-        for (int i = 0; i < n && delta < 0; i++) {
-          double t = c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr;
-          if (delta + t > 0) break;
-          delta += t;
+      }
+    } else if (gap < 0) {                     // scale_down: autoscaler.py:134-149
+      double delta = gap;
+      for (int i = 0; i < n && delta < 0; i++) {
+        const double t = n <= 32 ? __shfl_sync(FULL, thr, i)
+                                 : c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr;
+        if (delta + t > 0) break;
+        delta += t;
+        if (c.lane == 0) {
           c.sh->decisions++;
           remove_pod(c, c.t->s_ki[i]);
-          if (c.sh->err) break;
         }
+        if (failed(c)) break;
       }
     }
     if (failed(c)) return;

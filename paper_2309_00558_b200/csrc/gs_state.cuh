@@ -48,6 +48,7 @@ struct Layout {
   size_t s_carve;                                      // int4 [4R+8]
   size_t s_rs;                                         // int4 [4R+8] restructure list
   size_t s_pos;                                        // int2 [P] restructure positions
+  size_t s_fcur;                                       // i32 [F+1] per-function cursors (epoch)
   size_t bytes;
   int Q;
 };
@@ -98,6 +99,7 @@ __host__ __device__ inline Layout gs_make_layout(int G, int F, int P, int R, int
   take(L.s_carve, 4 * (size_t)R + 8, 16);
   take(L.s_rs, 4 * (size_t)R + 8, 16);
   take(L.s_pos, P, 8);
+  take(L.s_fcur, (size_t)F + 1, I);
   L.bytes = o;
   return L;
 }

@@ -993,21 +993,38 @@ __device__ void window_begin(Ctx& c, int w) {
     c.t->n_seg[g] = lo;
   }
   __syncwarp();
-  // per-function lists in (node, pod_id) order: stable counting sort
+  // per-function lists in (node, pod_id) order: stable counting sort,
+  // warp-parallel (match_any groups lanes of one function)
+  int* cur = c.t->s_fcur;
+  for (int f = c.lane; f <= c.F; f += 32) cur[f] = 0;
   if (c.lane == 0) {
     c.sh->n_reg = nr;
     c.sh->pod_steps += (long long)nr * c.T;
-    for (int f = 0; f <= c.F; f++) c.t->f_loff[f] = 0;
-    for (int i = 0; i < nr; i++) c.t->f_loff[c.t->p_fn[c.t->s_rl[i]] + 1]++;
-    for (int f = 0; f < c.F; f++) c.t->f_loff[f + 1] += c.t->f_loff[f];
-    for (int i = 0; i < nr; i++) {          // loff[f] doubles as the cursor...
-      int slot = c.t->s_rl[i];
-      c.t->s_fl[c.t->f_loff[c.t->p_fn[slot]]++] = slot;
-    }
-    for (int f = c.F; f > 0; f--) c.t->f_loff[f] = c.t->f_loff[f - 1];  // ...then shifts back
-    c.t->f_loff[0] = 0;
   }
   __syncwarp();
+  for (int i0 = 0; i0 < nr; i0 += 32) {
+    const int i = i0 + c.lane;
+    const int fn = i < nr ? c.t->p_fn[c.t->s_rl[i]] : -1;
+    const unsigned m = __match_any_sync(FULL, fn);
+    if (fn >= 0 && c.lane == __ffs(m) - 1) atomicAdd(&cur[fn], __popc(m));
+  }
+  __syncwarp();
+  if (c.lane == 0) {
+    int acc = 0;
+    for (int f = 0; f < c.F; f++) { c.t->f_loff[f] = acc; const int k = cur[f]; cur[f] = acc; acc += k; }
+    c.t->f_loff[c.F] = acc;
+  }
+  __syncwarp();
+  for (int i0 = 0; i0 < nr; i0 += 32) {
+    const int i = i0 + c.lane;
+    const int slot = i < nr ? c.t->s_rl[i] : -1;
+    const int fn = slot >= 0 ? c.t->p_fn[slot] : -1;
+    const unsigned m = __match_any_sync(FULL, fn);
+    if (fn >= 0) c.t->s_fl[cur[fn] + __popc(m & ((1u << c.lane) - 1u))] = slot;
+    __syncwarp();
+    if (fn >= 0 && c.lane == __ffs(m) - 1) cur[fn] += __popc(m);
+    __syncwarp();
+  }
 }
 
 // ----------------------------------------------------------------------------

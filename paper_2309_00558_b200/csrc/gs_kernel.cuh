@@ -646,39 +646,50 @@ __device__ void place_batch(Ctx& c) {
   }
   __syncwarp();
   warp_sort(c, nb);
-  for (int i = c.lane; i < nb; i += 32) c.t->s_batch[i] = c.t->s_ki[i];
+  // batch order + each entry's best_match inputs (function, w, h)
+  for (int i = c.lane; i < nb; i += 32) {
+    const int slot = c.t->s_ki[i];
+    c.t->s_batch[i] = slot;
+    c.t->s_ka[i] = ((unsigned long long)(unsigned)c.t->p_w[slot] << 32) | (unsigned)c.t->p_h[slot];
+    c.t->s_ki[i] = c.t->p_fn[slot];
+  }
   __syncwarp();
   // best_match is a pure function of (node state, function, w, h): once a
-  // request fails, identical requests fail too until a placement changes the
-  // state, so they are answered from a one-entry memo (same counters).
-  int memo_f = -1, memo_w = 0, memo_h = 0;
-  long long memo_scans = 0;
-  for (int i = 0; i < nb; i++) {
-    int slot = c.t->s_batch[i];
-    int f = c.t->p_fn[slot], pw = c.t->p_w[slot], ph = c.t->p_h[slot];
+  // request fails, the identical requests that follow it in the batch fail
+  // too (nothing changes in between), so a whole run of them is settled at
+  // once with the same counters (attempts, failures, rect scans, retry flag).
+  int i = 0;
+  while (i < nb) {
+    const int slot = c.t->s_batch[i];
     int4 chosen;
-    int g;
-    if (f == memo_f && pw == memo_w && ph == memo_h) {
-      g = -1;
-      if (c.lane == 0) c.sh->rect_scans += memo_scans;
-    } else {
-      long long before = c.sh->rect_scans;
-      g = best_match(c, slot, &chosen);
-      __syncwarp();
-      memo_scans = c.sh->rect_scans - before;
-    }
-    if (c.lane == 0) c.sh->attempts++;
-    if (g < 0) {
-      memo_f = f; memo_w = pw; memo_h = ph;
-      if (c.lane == 0) {
-        c.sh->win_failures++;
-        c.t->p_flags[slot] |= PF_RETRY;
-      }
-      __syncwarp();
+    const long long before = c.sh->rect_scans;
+    const int g = best_match(c, slot, &chosen);
+    __syncwarp();
+    if (g >= 0) {
+      if (c.lane == 0) c.sh->attempts++;
+      if (!place_pod(c, slot, g, chosen)) return;
+      i++;
       continue;
     }
-    memo_f = -1;
-    if (!place_pod(c, slot, g, chosen)) return;
+    const long long scans = c.sh->rect_scans - before;
+    const unsigned long long key_a = c.t->s_ka[i];
+    const int key_f = c.t->s_ki[i];
+    int j = nb;                                  // first later entry with another key
+    for (int k0 = i + 1; k0 < nb; k0 += 32) {
+      const int k = k0 + c.lane;
+      const bool differs = k < nb && (c.t->s_ka[k] != key_a || c.t->s_ki[k] != key_f);
+      const unsigned bal = __ballot_sync(FULL, differs);
+      if (bal) { j = k0 + __ffs(bal) - 1; break; }
+    }
+    for (int k = i + c.lane; k < j; k += 32) c.t->p_flags[c.t->s_batch[k]] |= PF_RETRY;
+    if (c.lane == 0) {
+      const int len = j - i;
+      c.sh->attempts += len;
+      c.sh->win_failures += len;
+      c.sh->rect_scans += scans * (len - 1);
+    }
+    __syncwarp();
+    i = j;
   }
   __syncwarp();
 }

@@ -51,6 +51,10 @@ struct Hot {
   int seg[GC + 1];
   int cut[GC];
   unsigned long long covbits[GC];
+  // per step: requesting SM (integral), grants, 1 = dispatch order changed /
+  // 2 = a partial token; occupancy-sum cache of the last all-quantum step
+  int reqsm[GC], ngr[GC], ostate[GC], occn[GC];
+  double occv[GC];
   int nplaced[GC];
   double fp[GC];
   // run constants (so the step loop needs no Ctx registers)
@@ -131,7 +135,7 @@ __device__ bool hot_load(Ctx& c, H* h) {
   }
   for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.t->f_loff[f];
   for (int g = c.lane; g < c.G; g += 32) {
-    h->sr[g] = c.t->n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0;
+    h->sr[g] = c.t->n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0; h->occn[g] = -1;
     h->nplaced[g] = c.t->n_nplaced[g]; h->fp[g] = c.t->n_fp[g];
   }
   for (int g = c.lane; g <= c.G; g += 32) h->seg[g] = c.t->n_seg[g];
@@ -459,7 +463,10 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   for (int f = lane; f < F; f += 32) hot_admit(h, f, t0);
   if (s > 0 && !integral) hot_complete_sm(h, lane);
 #pragma unroll 1
-  for (int g = lane; g < G; g += 32) { h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull; }
+  for (int g = lane; g < G; g += 32) {
+    h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull;
+    h->reqsm[g] = 0; h->ngr[g] = 0; h->ostate[g] = 0;
+  }
   __syncwarp();
   // complete live tokens + filter_pods + requesting:
   // key = -(q_req - q_used) for requesting pods, ~0 otherwise
@@ -478,6 +485,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
     h->key[i] = req ? ord_key(-(h->qreq[i] - qused)) : ~0ull;
+    if (req && integral) atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
     any_req |= req;
   }
   // No pod requests a token: dispatch grants nothing, so coverage, occupancy,
@@ -497,17 +505,30 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const unsigned long long k = h->key[i];
     const int lo = h->seg[g], hi = h->seg[g + 1];
     int r = 0;
-    double ahead = 0.0;
+    // the SM sum ahead is only needed when the node's requesting SM can
+    // exceed 100 (otherwise no requesting pod misfits)
+    const bool need_ahead = integral && k != ~0ull && h->reqsm[g] > (int)SM_LIMIT;
+    if (need_ahead) {
+      double ahead = 0.0;
 #pragma unroll 1
-    for (int j = lo; j < hi; j++) {
-      const unsigned long long kj = h->key[j];
-      const bool less = (kj < k) || (kj == k && j < i);
-      r += less;
-      if (less) ahead += h->sm[j];
+      for (int j = lo; j < hi; j++) {
+        const unsigned long long kj = h->key[j];
+        const bool less = (kj < k) || (kj == k && j < i);
+        r += less;
+        if (less) ahead += h->sm[j];
+      }
+      if (h->sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], r);
+    } else {
+#pragma unroll 1
+      for (int j = lo; j < hi; j++) {
+        const unsigned long long kj = h->key[j];
+        r += (kj < k) || (kj == k && j < i);
+      }
     }
+    // (each order position is read and written only by the lane whose pod lands there)
+    if (integral && k != ~0ull && h->order[lo + r] != (short)i) atomicOr(&h->ostate[g], 1);
     h->order[lo + r] = (short)i;
     h->rank[i] = (short)r;
-    if (integral && k != ~0ull && h->sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], r);
   }
   __syncwarp();
   const double quantum = h->quantum;
@@ -521,6 +542,8 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
         const double dur = rem < quantum ? rem : quantum;
         h->flags[i] |= PF_GRANT;
         atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
+        atomicAdd(&h->ngr[g], 1);
+        if (rem < quantum) atomicOr(&h->ostate[g], 2);
         grants++;
       }
     }
@@ -528,19 +551,27 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     // occupancy: Python sum() of sm*duration in dispatch order, per node
 #pragma unroll 1
     for (int g = lane; g < G; g += 32) {
-      PySum occ;
-      occ.reset();
-      const int e = h->seg[g + 1];
+      const int ng = h->ngr[g];                // granted = dispatch positions [0, ng)
+      if (ng == 0) { h->occn[g] = -1; continue; }   // order rewritten, cache not refreshed
+      const int st = h->ostate[g];
+      double v;
+      if (st == 0 && ng == h->occn[g]) {
+        v = h->occv[g];   // same pods, same order, all full-quantum tokens: same terms
+      } else {
+        PySum occ;
+        occ.reset();
+        const int lo = h->seg[g];
 #pragma unroll 1
-      for (int j = h->seg[g]; j < e; j++) {
-        const int i = h->order[j];
-        if (!(h->flags[i] & PF_GRANT)) break;
-        occ.add(h->sm[i] * h->dur(i));
+        for (int j = lo; j < lo + ng; j++) {
+          const int i = h->order[j];
+          occ.add(h->sm[i] * h->dur(i));
+        }
+        v = occ.value() / 100.0;
+        h->occv[g] = v;
+        h->occn[g] = (st & 2) ? -1 : ng;
       }
-      if (occ.n) {
-        h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
-        h->occ[g] += occ.value() / 100.0;
-      }
+      h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
+      h->occ[g] += v;
     }
   } else {
     grants = hot_dispatch_float(h, lane);

@@ -29,14 +29,17 @@ enum : int { GS_CAP_HOT = 5 };   // status detail: working set exceeds the size 
 template <int PC_, int FC_, int GC_>
 struct Hot {
   static constexpr int PC = PC_, FC = FC_, GC = GC_;
+  static_assert(PC <= 256, "pod indices are stored in bytes");
   // registered pods of this window, in (node, pod_id) order
   // (a granted pod's duration min(quantum, q_lim - q_used) is recomputed where
   // needed: q_used does not change between dispatch and completion)
   double qused[PC], qreq[PC], qlim[PC], sm[PC], busy[PC], crem[PC], carr[PC], invr[PC];
   unsigned long long key[PC];
   long long cur[PC];
-  int fnode[PC], flags[PC];
-  short order[PC], flist[PC], rank[PC];   // rank doubles as the serve phase's granted list
+  int fnode[PC];
+  // pod indices (PC <= 256) and flag bits (PF_CUR | PF_GRANT) fit in a byte
+  unsigned char flags[PC];
+  unsigned char order[PC], flist[PC], rank[PC];   // rank doubles as the serve phase's granted list
   // functions
   double farr[FC], slo[FC];
   int qlen[FC], pinned[FC], fw[FC], fi[FC], fcnt[FC], nsn[FC], nsw[FC], nsi[FC];
@@ -86,7 +89,7 @@ struct Hot {
 };
 
 // size classes: (pods, functions, nodes)
-typedef Hot<64, 16, 8> HotS;
+typedef Hot<64, 12, 4> HotS;
 typedef Hot<128, 32, 16> HotM;
 typedef Hot<256, 64, 32> HotL;
 
@@ -116,8 +119,8 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->invr[i] = c.t->p_invr[s];
     h->cur[i] = pack_id(c.t->p_cw[s], c.t->p_ci[s]);
     h->fnode[i] = c.t->p_fn[s] | (c.t->p_node[s] << 16);
-    h->flags[i] = c.t->p_flags[s] & PF_CUR;
-    h->order[i] = (short)i;
+    h->flags[i] = (unsigned char)(c.t->p_flags[s] & PF_CUR);
+    h->order[i] = (unsigned char)i;
   }
   for (int f = c.lane; f < c.F; f += 32) {
     h->qlen[f] = c.t->f_qlen[f]; h->pinned[f] = c.t->f_pinned[f];
@@ -152,7 +155,7 @@ __device__ bool hot_load(Ctx& c, H* h) {
   // index of an arena slot is its position in s_rl (slot -> index via s_list).
   for (int i = c.lane; i < n; i += 32) c.t->s_list[c.t->s_rl[i]] = i;
   __syncwarp();
-  for (int j = c.lane; j < n; j += 32) h->flist[j] = (short)c.t->s_list[c.t->s_fl[j]];
+  for (int j = c.lane; j < n; j += 32) h->flist[j] = (unsigned char)c.t->s_list[c.t->s_fl[j]];
   __syncwarp();
   return true;
 }
@@ -214,7 +217,7 @@ __device__ __forceinline__ void hot_complete(H* h, int lane) {
     const int fl = h->flags[i];
     if (fl & PF_GRANT) {
       h->qused[i] += h->dur(i);
-      h->flags[i] = fl & ~PF_GRANT;
+      h->flags[i] = (unsigned char)(fl & ~PF_GRANT);
     }
   }
 }
@@ -317,7 +320,7 @@ __device__ __forceinline__ void hot_serve(H* h, int i, int f, double t_start, do
   h->busy[i] = t;
   h->crem[i] = rem;
   h->carr[i] = arr;
-  h->flags[i] = fl;
+  h->flags[i] = (unsigned char)fl;
   h->wcomp[f] += comp;
   h->wviol[f] += viol;
 }
@@ -407,7 +410,7 @@ __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start,
   h->busy[i] = t;
   h->crem[i] = rem;
   h->carr[i] = arr;
-  h->flags[i] = fl;
+  h->flags[i] = (unsigned char)fl;
 }
 
 // dispatch for non-integral SM partitions: the sequential head-blocking walk
@@ -480,7 +483,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       qused += h->dur(i);
       h->qused[i] = qused;
       fl &= ~PF_GRANT;
-      h->flags[i] = fl;
+      h->flags[i] = (unsigned char)fl;
     }
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
@@ -526,9 +529,9 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       }
     }
     // (each order position is read and written only by the lane whose pod lands there)
-    if (integral && k != ~0ull && h->order[lo + r] != (short)i) atomicOr(&h->ostate[g], 1);
-    h->order[lo + r] = (short)i;
-    h->rank[i] = (short)r;
+    if (integral && k != ~0ull && (int)h->order[lo + r] != i) atomicOr(&h->ostate[g], 1);
+    h->order[lo + r] = (unsigned char)i;
+    h->rank[i] = (unsigned char)r;
   }
   __syncwarp();
   const double quantum = h->quantum;
@@ -594,7 +597,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const int i = j < n ? h->flist[j] : 0;
     const bool gr = j < n && (h->flags[i] & PF_GRANT);
     const unsigned bal = __ballot_sync(FULL, gr);
-    if (gr) h->rank[ngl + __popc(bal & ((1u << lane) - 1u))] = (short)i;
+    if (gr) h->rank[ngl + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)i;
     ngl += __popc(bal);
   }
   __syncwarp();

@@ -25,7 +25,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__registers_per_thread",
         "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed.sum"]
-summary = {"tag": tag, "kernel": "gs_sim_kernel<Hot<64,16,8>>",
+summary = {"tag": tag, "kernel": "gs_sim_kernel<Hot<64,12,4>>",
            "command": "ncu --set full --clock-control none --import-source on -k regex:gs_sim_kernel -c 1 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e",
            "metrics": {k: raw[k][0] + (" " + raw[k][1] if raw[k][1] else "") for k in keys if k in raw}}
 summary["dram_bytes_per_launch"] = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
@@ -43,6 +43,8 @@ summary["launch_list"] = {"launches": len(launches), "gs_sim_kernel_launches": s
                           "note": "cold-cache serialised ncu times; the L2-flush fill kernels are bench.py's, outside the timed region"}
 stall = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_hot.py"), rep, "0"], capture_output=True, text=True).stdout
 lines_out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, so, "25"], capture_output=True, text=True).stdout
+funcs_out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_funcs.py"), rep, so, "HotILi64", "30"], capture_output=True, text=True).stdout
+regions_out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_regions.py"), rep, so, "HotILi64", "0"], capture_output=True, text=True).stdout
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 with open(os.path.join(ROOT, "profiles", "ncu_c2_summary.json"), "w") as fh:
     json.dump(summary, fh, indent=1)
@@ -52,6 +54,8 @@ if len(sys.argv) > 2 and os.path.exists(sys.argv[2]):
 with open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w") as fh:
     fh.write(f"# ncu summary {tag}: scenario megakernel on C2 (9472 runs x 300 windows)\n\n")
     fh.write("```\n" + json.dumps(summary, indent=1) + "\n```\n\n## stall reasons\n\n```\n" + stall + "```\n\n")
+    fh.write("## code regions (quantum-step subroutine vs window/epoch code)\n\n```\n" + regions_out + "```\n\n")
+    fh.write("## per function (samples / executed instructions)\n\n```\n" + funcs_out + "```\n\n")
     fh.write("## hottest source lines (samples / executed instructions)\n\n```\n" + lines_out + "```\n")
     if bench:
         fh.write("\n## bench.py line of the same round\n\n```\n" + bench + "\n```\n")

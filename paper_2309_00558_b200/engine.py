@@ -113,13 +113,15 @@ def _normalise(scenarios, policies):
     return scenarios, policies
 
 
-def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
-             rows: bool = True, caps: cc.Caps | None = None) -> list:
-    """Run a batch of (scenario, policy) pairs on the GPU.
+def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
+                     caps: cc.Caps | None = None) -> list:
+    """Run a batch of (scenario, policy) pairs on the GPU; raw device records.
 
-    Returns one ``RunResult`` per input (or the exception, when
-    ``errors="return"``).  Runs that outgrow a static device capacity are
-    re-executed on the device with doubled capacities; nothing is truncated.
+    Returns one ``(batch, out, r)`` handle per input -- run ``r`` of the
+    compiled ``batch`` whose output arrays are ``out`` -- or the exception
+    (``errors="return"``).  Runs that outgrow a static device capacity are
+    re-executed on the device with enlarged capacities; nothing is truncated.
+    ``decode_run`` / ``report.run_csv`` turn a handle into report rows.
     """
     from . import backend
     scenarios, policies = _normalise(scenarios, policies)
@@ -143,9 +145,10 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
             st = out["status"][j]
             if int(st["code"]) == cc.GS_ERR_CAPACITY:
                 rr = batch.runs[j]
-                caps = cc.Caps(int(rr["cap_pods"]), int(rr["cap_rects"]), int(rr["cap_returned"]),
-                               int(rr["hot_class"])).grown(int(st["detail"]), int(st["hot_class"]))
-                images[i] = cc.compile_run(scenarios[i], policies[i], caps)
+                caps_j = cc.Caps(int(rr["cap_pods"]), int(rr["cap_rects"]),
+                                 int(rr["cap_returned"]), int(rr["hot_class"])
+                                 ).grown(int(st["detail"]), int(st["hot_class"]))
+                images[i] = cc.compile_run(scenarios[i], policies[i], caps_j)
                 retry.append(i)
                 continue
             err = run_error(batch.images[j], st)
@@ -154,7 +157,7 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
                     raise err
                 results[i] = err
             else:
-                results[i] = decode_run(batch, j, out)
+                results[i] = (batch, out, j)
         pending = retry
     for i in pending:
         err = CapacityError("run still exceeds device capacities after "
@@ -163,6 +166,18 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
             raise err
         results[i] = err
     return results
+
+
+def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
+             rows: bool = True, caps: cc.Caps | None = None) -> list:
+    """Run a batch of (scenario, policy) pairs on the GPU.
+
+    Returns one ``RunResult`` per input (or the exception, when
+    ``errors="return"``).  Runs that outgrow a static device capacity are
+    re-executed on the device with doubled capacities; nothing is truncated.
+    """
+    recs = simulate_records(scenarios, policies, device=device, errors=errors, caps=caps)
+    return [r if isinstance(r, Exception) else decode_run(*r) for r in recs]
 
 
 def run_batch(scenarios, policies="fast", *, device: int = 0, errors: str = "raise") -> list:

@@ -180,15 +180,36 @@ def _resource_config_check(sm, q_req, q_lim):
         raise ValidationError(f"quota_request {q_req!r} exceeds quota_limit {q_lim!r}")
 
 
+def _profile_memo(profile) -> dict:
+    """Per-profile-object cache of compile-time derived data (profiles are
+    immutable inputs; sweeps share one object per synth spec, scenario.py)."""
+    memo = getattr(profile, "_gs_memo", None)
+    if memo is None:
+        memo = {}
+        try:
+            object.__setattr__(profile, "_gs_memo", memo)
+        except (AttributeError, TypeError):       # slotted / foreign objects: no cache
+            pass
+    return memo
+
+
+def _t_eff(profile) -> float:
+    memo = _profile_memo(profile)
+    t = memo.get("t_eff")
+    if t is None:
+        pts = list(profile.entries.values())
+        rpr_best = min(pts, key=lambda e: (-(e.throughput_rps / e.point.resource_area),
+                                           e.point.resource_area, e.point.sm_partition,
+                                           e.point.quota))
+        t = memo["t_eff"] = max(rpr_best.throughput_rps, 1e-9)
+    return t
+
+
 def _default_caps(scenario, fns) -> Caps:
     window_s = scenario.window_ms / 1000.0
     pods = 8
     for fn in fns:
-        pts = list(fn.profile.entries.values())
-        rpr_best = min(pts, key=lambda e: (-(e.throughput_rps / e.point.resource_area),
-                                           e.point.resource_area, e.point.sm_partition,
-                                           e.point.quota))
-        t_eff = max(rpr_best.throughput_rps, 1e-9)
+        t_eff = _t_eff(fn.profile)
         counts = fn.trace.counts[:scenario.windows]
         peak = max(counts, default=0) / window_s
         pods += len(fn.initial_pods) + int(math.ceil(1.5 * peak / t_eff)) + 4
@@ -207,14 +228,27 @@ class _LoweredProfile:
     h_den: tuple
     p_eff: int
     sm_integral: bool
+    lx: int                 # lcm of the width / height denominators
+    ly: int
 
 
 _LOWER_CACHE: dict = {}
 
 
 def _lower_profile(profile, timeshare: bool) -> _LoweredProfile:
-    """Policy-specific dense point table of one profile (cached by content:
-    sweeps reuse a handful of profiles across thousands of scenarios)."""
+    """Policy-specific dense point table of one profile (cached on the profile
+    object, then by content: sweeps reuse a handful of profiles across
+    thousands of scenarios)."""
+    memo = _profile_memo(profile)
+    hit = memo.get(("lower", timeshare))
+    if hit is not None:
+        return hit
+    lo = _lower_profile_content(profile, timeshare)
+    memo[("lower", timeshare)] = lo
+    return lo
+
+
+def _lower_profile_content(profile, timeshare: bool) -> _LoweredProfile:
     pts = sorted(profile.entries)
     ckey = (timeshare, tuple((p.sm_partition, p.quota, profile.entries[p].throughput_rps)
                              for p in pts))
@@ -245,7 +279,8 @@ def _lower_profile(profile, timeshare: bool) -> _LoweredProfile:
         if best is None or key < best[0]:
             best = (key, i)
     lo = _LoweredProfile(keys, {k: i for i, k in enumerate(keys)}, rows, tuple(w_num),
-                         tuple(w_den), tuple(h_num), tuple(h_den), best[1], integral)
+                         tuple(w_den), tuple(h_num), tuple(h_den), best[1], integral,
+                         reduce(_lcm, w_den, 1), reduce(_lcm, h_den, 1))
     if len(_LOWER_CACHE) > 4096:
         _LOWER_CACHE.clear()
     _LOWER_CACHE[ckey] = lo
@@ -302,8 +337,8 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
 
     lowered = [_lower_profile(fn.profile, timeshare) for fn in fns]
     # geometry scale: every as_frac(quota)*100 / as_frac(sm_eff) becomes integral
-    lx = reduce(_lcm, (d for lo in lowered for d in lo.w_den), 1)
-    ly = reduce(_lcm, (d for lo in lowered for d in lo.h_den), 1)
+    lx = reduce(_lcm, (lo.lx for lo in lowered), 1)
+    ly = reduce(_lcm, (lo.ly for lo in lowered), 1)
     side_x, side_y = 100 * lx, 100 * ly
     n_nodes = int(scenario.fleet_size)
     if (side_x > _MAX_SIDE or side_y > _MAX_SIDE

@@ -7,6 +7,8 @@ accepts the reference's own ``Scenario`` objects by duck typing.
 """
 from __future__ import annotations
 
+import functools
+
 import json
 import math
 import os
@@ -168,6 +170,16 @@ def _point(sm, q, fn):
     return cls(sm, q)
 
 
+@functools.lru_cache(maxsize=4096)
+def _synth_cached(fid, t_max, knee, grid_sm, grid_q, slo_ms, mem_items):
+    """One FunctionProfile object per distinct synth spec: profiles are
+    immutable inputs, and sharing the object lets the compiler reuse its
+    lowered point table across the scenarios of a sweep."""
+    mem = MemorySpec(**dict(mem_items)) if mem_items else None
+    return synth_profile(fid, t_max, knee, grid_points(list(grid_sm), list(grid_q)),
+                         slo_latency_ms=slo_ms, mem=mem)
+
+
 def _function_from_dict(data: dict, scenario: dict, base_dir: str | None) -> FunctionSpec:
     fid = data.get("function_id")
     if not fid:
@@ -177,11 +189,11 @@ def _function_from_dict(data: dict, scenario: dict, base_dir: str | None) -> Fun
         raise ValidationError(f"{fid}: function entry needs a profile object")
     if "synth" in prof:
         s = prof["synth"]
-        mem = MemorySpec(**s["mem"]) if s.get("mem") else None
-        grid = grid_points(s.get("grid_sm", DEFAULT_SM_GRID),
-                           s.get("grid_quota", DEFAULT_QUOTA_GRID))
-        profile = synth_profile(fid, float(s["t_max"]), float(s["sm_knee"]), grid,
-                                slo_latency_ms=float(s.get("slo_ms", 1000.0)), mem=mem)
+        profile = _synth_cached(fid, float(s["t_max"]), float(s["sm_knee"]),
+                                tuple(s.get("grid_sm", DEFAULT_SM_GRID)),
+                                tuple(s.get("grid_quota", DEFAULT_QUOTA_GRID)),
+                                float(s.get("slo_ms", 1000.0)),
+                                tuple(sorted(s["mem"].items())) if s.get("mem") else None)
     elif "csv" in prof:
         path = prof["csv"]
         if base_dir is not None and not os.path.isabs(path):

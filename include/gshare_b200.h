@@ -216,6 +216,23 @@ int gs_session_last_launches(gs_session_t* sess);
 double gs_session_last_kernel_ms(gs_session_t* sess);
 void gs_session_destroy(gs_session_t* sess);
 
+/* Packer auditor (the reference's check_node, packer.py:327-388, decided
+ * exactly on the scaled integer grid compressed to the rectangle edges): per
+ * run, the OR over its nodes of GS_AUDIT_* bits for the final geometry. */
+#define GS_AUDIT_PLACED_OVERLAP 1u   /* two placements intersect            */
+#define GS_AUDIT_FREE_PLACED    2u   /* a free rect intersects a placement  */
+#define GS_AUDIT_FREE_CONTAINED 4u   /* a free rect inside another          */
+#define GS_AUDIT_GAP            8u   /* area neither free nor placed        */
+#define GS_AUDIT_DOUBLE        16u   /* area both free and placed           */
+#define GS_AUDIT_TOO_BIG       32u   /* > 256 rects on a node: not audited  */
+int gs_session_audit(gs_session_t* sess, uint32_t* breaches /* [n_runs] */, void* stream,
+                     char* err, size_t err_len);
+/* The same audit on caller geometry: node k holds n_free[k] free then
+ * n_placed[k] placed (x, y, w, h) int32 rects at rects[4*cap*k ...]. */
+int gs_audit_geometry(const int32_t* rects, const int32_t* n_free, const int32_t* n_placed,
+                      int n_nodes, int cap, int side_x, int side_y, uint32_t* breaches,
+                      int device, char* err, size_t err_len);
+
 /* Launch shape (0 = default).  warps_per_block: scenario warps per CTA. */
 int gs_set_launch(int warps_per_block, int blocks_per_sm);
 

@@ -54,6 +54,10 @@ def lib():
             L.gs_set_launch.restype = i
             L.gs_session_upload.argtypes = [vp, vp, vp, cp, sz]
             L.gs_session_upload.restype = i
+            L.gs_session_audit.argtypes = [vp, vp, vp, cp, sz]
+            L.gs_session_audit.restype = i
+            L.gs_audit_geometry.argtypes = [vp, vp, vp, i, i, i, i, vp, i, cp, sz]
+            L.gs_audit_geometry.restype = i
             L.gs_session_map_host.argtypes = [vp, vp]
             L.gs_session_map_host.restype = i
             L.gs_host_alloc.argtypes = [sz, C.POINTER(vp)]
@@ -167,6 +171,16 @@ class Session:
         _check(rc, err, "gs_session_download")
         return out
 
+    def audit(self, stream=None):
+        """Packer audit of every run's final geometry: uint32 GS_AUDIT_* bits
+        per run (0 = the reference's check_node finds nothing)."""
+        import numpy as np
+        out = np.zeros(len(self.batch), np.uint32)
+        err = C.create_string_buffer(512)
+        rc = self._lib.gs_session_audit(self.handle, out.ctypes.data, stream, err, len(err))
+        _check(rc, err, "gs_session_audit")
+        return out
+
     def launches(self) -> int:
         return self._lib.gs_session_last_launches(self.handle)
 
@@ -194,6 +208,34 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+AUDIT_BITS = {1: "placed_overlap", 2: "free_placed", 4: "free_contained", 8: "gap",
+              16: "double", 32: "too_big"}
+
+
+def audit_geometry(nodes, side_x: int, side_y: int, device: int = 0):
+    """Run the device packer auditor on explicit geometry.
+
+    ``nodes``: list of (free_rects, placed_rects), rects as (x, y, w, h) ints.
+    Returns one uint32 of GS_AUDIT_* bits per node."""
+    import numpy as np
+    cap = max([1] + [len(f) + len(p) for f, p in nodes])
+    rects = np.zeros((len(nodes), cap, 4), np.int32)
+    nf = np.zeros(len(nodes), np.int32)
+    npl = np.zeros(len(nodes), np.int32)
+    for k, (free, placed) in enumerate(nodes):
+        allr = list(free) + list(placed)
+        if allr:
+            rects[k, :len(allr)] = np.asarray(allr, np.int32)
+        nf[k], npl[k] = len(free), len(placed)
+    out = np.zeros(len(nodes), np.uint32)
+    err = C.create_string_buffer(512)
+    rc = lib().gs_audit_geometry(rects.ctypes.data, nf.ctypes.data, npl.ctypes.data,
+                                 len(nodes), cap, int(side_x), int(side_y), out.ctypes.data,
+                                 int(device), err, len(err))
+    _check(rc, err, "gs_audit_geometry")
+    return out
 
 
 def set_launch(warps_per_block: int = 0, blocks_per_sm: int = -1):

@@ -14,6 +14,7 @@
 
 #include "gs_kernel.cuh"
 #include "gs_hot.cuh"
+#include "gs_audit.cuh"
 
 namespace gs {
 
@@ -684,6 +685,74 @@ extern "C" int gs_session_download(gs_session_t* s, const gs_out_t* out, void* s
   int worst = GS_OK;
   for (int r = 0; r < s->n_runs; r++) worst = std::max(worst, (int)out->status[r].code);
   return worst;
+}
+
+// Packer audit of every run's final node geometry: breach
+// bits (GS_AUDIT_*) OR-ed over the run's nodes, one uint32 per run.
+extern "C" int gs_session_audit(gs_session_t* s, uint32_t* breaches, void* stream_ptr,
+                                char* err, size_t err_len) {
+  if (!s || !breaches) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
+  CK(cudaSetDevice(s->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
+  const int R = s->n_runs;
+  if (R == 0) return GS_OK;
+  const int blocks = (R + 3) / 4;
+  gs_batch_t* d_in = nullptr;
+  int4* scratch = nullptr;
+  unsigned* d_out = nullptr;
+  CK(cudaMalloc(&d_in, sizeof(gs_batch_t)));
+  CK(cudaMalloc(&scratch, sizeof(int4) * (size_t)blocks * 4 * AUD_MAX_RECTS));
+  CK(cudaMalloc(&d_out, sizeof(unsigned) * (size_t)R));
+  CK(cudaMemcpyAsync(d_in, &s->dev_in, sizeof(gs_batch_t), cudaMemcpyHostToDevice, st));
+  AuditArgs a{};
+  a.in = d_in; a.arena = s->arena; a.ws_off = s->ws_off; a.n_runs = R;
+  a.scratch = scratch; a.out = d_out;
+  gs_audit_session_kernel<<<blocks, 128, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(breaches, d_out, sizeof(unsigned) * (size_t)R,
+                                            cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_in); cudaFree(scratch); cudaFree(d_out);
+  CK(e);
+  return GS_OK;
+}
+
+// The same auditor on caller-supplied geometry (host buffers): node k has
+// n_free[k] free rects then n_placed[k] placed rects at rects[k*cap*4 ...]
+// as (x, y, w, h) int32 quadruples on a side_x x side_y plane.
+extern "C" int gs_audit_geometry(const int32_t* rects, const int32_t* n_free,
+                                 const int32_t* n_placed, int n_nodes, int cap, int side_x,
+                                 int side_y, uint32_t* breaches, int device, char* err,
+                                 size_t err_len) {
+  if (!rects || !n_free || !n_placed || !breaches || n_nodes < 0 || cap < 1) {
+    put_err(err, err_len, "bad arguments");
+    return GS_ERR_ARG;
+  }
+  if (n_nodes == 0) return GS_OK;
+  CK(cudaSetDevice(device));
+  int4* d_r = nullptr;
+  int *d_f = nullptr, *d_p = nullptr;
+  unsigned* d_o = nullptr;
+  const size_t nr = (size_t)n_nodes * cap;
+  CK(cudaMalloc(&d_r, sizeof(int4) * nr));
+  CK(cudaMalloc(&d_f, sizeof(int) * (size_t)n_nodes));
+  CK(cudaMalloc(&d_p, sizeof(int) * (size_t)n_nodes));
+  CK(cudaMalloc(&d_o, sizeof(unsigned) * (size_t)n_nodes));
+  cudaError_t e = cudaMemcpy(d_r, rects, sizeof(int4) * nr, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_f, n_free, sizeof(int) * n_nodes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_p, n_placed, sizeof(int) * n_nodes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    AuditArgs a{};
+    a.rects = d_r; a.nfree = d_f; a.nplaced = d_p; a.cap = cap; a.n_nodes = n_nodes;
+    a.side_x = side_x; a.side_y = side_y; a.out = d_o;
+    gs_audit_geometry_kernel<<<(n_nodes + 3) / 4, 128>>>(a);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(breaches, d_o, sizeof(unsigned) * n_nodes,
+                                       cudaMemcpyDeviceToHost);
+  cudaFree(d_r); cudaFree(d_f); cudaFree(d_p); cudaFree(d_o);
+  CK(e);
+  return GS_OK;
 }
 
 extern "C" int gs_session_device_out(gs_session_t* s, gs_out_t* dev_out) {

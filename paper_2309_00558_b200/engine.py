@@ -177,7 +177,7 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
     re-executed on the device with doubled capacities; nothing is truncated.
     """
     recs = simulate_records(scenarios, policies, device=device, errors=errors, caps=caps)
-    return [r if isinstance(r, Exception) else decode_run(*r) for r in recs]
+    return [r if isinstance(r, Exception) else decode_run(r[0], r[2], r[1]) for r in recs]
 
 
 def run_batch(scenarios, policies="fast", *, device: int = 0, errors: str = "raise") -> list:

@@ -76,3 +76,19 @@ def test_capacity_overflow_is_retried_not_truncated():
     ref_batch = cc.Batch([cc.compile_run(sc, "fast")])
     want = engine.decode_run(ref_batch, 0, oracle.run_batch(ref_batch))
     assert diff_results(res, want) == ""
+
+
+def test_gpu_matches_oracle_c4_large_fleet():
+    # 64 nodes x 200 functions (BASELINE configs[3]): the HBM-arena (XL) path
+    scen = [Scenario.from_dict(wl.c4(s, windows=40)) for s in range(3)]
+    assert_gpu_matches_oracle(scen, ["fast"] * len(scen))
+
+
+def test_gpu_matches_oracle_c2_timeshare_and_mixed_classes():
+    # one batch mixing every size class the launcher dispatches (S/M/L/XL)
+    scen = [Scenario.from_dict(wl.c2(s, windows=30)) for s in range(6)]
+    scen += [Scenario.from_dict(wl.c2(s, windows=30, n_funcs=20, fleet=8)) for s in range(4)]
+    scen += [Scenario.from_dict(wl.c2(s, windows=20, n_funcs=48, fleet=24)) for s in range(2)]
+    scen += [Scenario.from_dict(wl.c4(s, windows=12, n_funcs=80, fleet=40)) for s in range(2)]
+    pols = ["fast", "timeshare"] * 7
+    assert_gpu_matches_oracle(scen, pols)

@@ -161,7 +161,7 @@ def cpu_reference(batch, sample_runs: int, threads: int):
 def cpu_sample_size(batch, threads: int, target_s: float) -> int:
     """Runs of `batch` the oracle finishes in about `target_s` seconds on
     `threads` host threads (calibrated on a small prefix)."""
-    n0 = min(len(batch), max(2 * threads, 32))
+    n0 = min(len(batch), max(4 * threads, 64))
     _, dt, _ = cpu_reference(batch, n0, threads)
     return int(min(len(batch), max(n0, n0 * target_s / max(dt, 1e-3))))
 
@@ -239,12 +239,12 @@ def run_reference_arm(args, rank, world):
     batch = build_batch(range(sample), args.windows) if sample > len(pool) else pool
     for _ in range(args.warmup):
         cpu_reference(batch, min(sample, 2 * threads), threads)
-    times, vals = [], []
+    times, simsec = [], []
     for _ in range(args.steps):
-        v, dt, sub = cpu_reference(batch, sample, threads)
-        vals.append(v)
+        _, dt, sub = cpu_reference(batch, sample, threads)
+        simsec.append(sim_seconds(sub))           # the sample actually simulated
         times.append(dt)
-    value = sum(sim_seconds(batch) for _ in vals) / sum(times)
+    value = sum(simsec) / sum(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,

@@ -65,7 +65,7 @@ struct Hot {
   long long* f_ret;
   long long* f_ring;
   double ws, qs, quantum;
-  int n, F, G, T, W, RET, integral;
+  int n, F, G, T, W, RET, integral, bounded;
 
   __device__ __forceinline__ int count(int f, int w) const { return counts[coff[f] + w]; }
   // token duration of a granted pod: min(quantum, q_limit - q_used) (token_backend.py:178)
@@ -149,6 +149,9 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
     h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
     h->integral = c.integral() ? 1 : 0;
+    int bnd = 0;
+    for (int f = 0; f < c.F; f++) bnd |= c.fs[f].max_queue >= 0;
+    h->bounded = bnd;
   }
   __syncwarp();
   // s_fl holds arena slots in (node, pod_id) order per function; the hot
@@ -222,7 +225,7 @@ __device__ __forceinline__ void hot_complete(H* h, int lane) {
   }
 }
 
-template <class H>
+template <class H, bool BND>
 __device__ __forceinline__ void hot_admit(H* h, int f, double t0) {
   int cnt = h->fcnt[f];
   if (cnt == 0) return;
@@ -230,7 +233,7 @@ __device__ __forceinline__ void hot_admit(H* h, int f, double t0) {
   const double now = t0 + TIME_EPS;
   if (!(a <= now)) return;
   int w = h->fw[f], i = h->fi[f], wn = h->fwn[f];
-  const int limit = h->maxq[f];
+  const int limit = BND ? h->maxq[f] : -1;
   int qlen = h->qlen[f], nsn = h->nsn[f], drop = 0;
   #pragma unroll 1
   while (true) {
@@ -328,7 +331,7 @@ __device__ __forceinline__ void hot_serve(H* h, int i, int f, double t_start, do
 // id of the `pos`-th unpinned request of function f at the start of the serve
 // phase: restarted (returned) requests first, then never-started ones in
 // queue order (sim_engine.py:531 takes the first request with server None).
-template <class H>
+template <class H, bool BND>
 __device__ __forceinline__ double unpinned_at(const H* h, int f, int pos, long long* id_out) {
   const int retn = h->retn[f];
   if (pos < retn) {
@@ -337,7 +340,7 @@ __device__ __forceinline__ double unpinned_at(const H* h, int f, int pos, long l
     return h->arrival(f, id_w(id), id_i(id));
   }
   const int q = pos - retn;
-  const int limit = h->maxq[f];
+  const int limit = BND ? h->maxq[f] : -1;
   if (limit >= 0) {
     const long long id = h->f_ring[h->ringoff[f] + (h->rhead[f] + q) % limit];
     *id_out = id;
@@ -376,7 +379,7 @@ __device__ __forceinline__ int serve_dry_run(const H* h, int i, double t_start, 
 
 // _serve (sim_engine.py:525-552) for pod i whose k-th new request is the
 // (base+k)-th unpinned one and which may start at most `avail` requests.
-template <class H>
+template <class H, bool BND>
 __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start, double t_end,
                                              int base, int avail, int& comp, int& viol) {
   const double busy = h->busy[i];
@@ -391,7 +394,7 @@ __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start,
     if (!(fl & PF_CUR)) {
       if (taken == avail) break;                 // queue ran dry
       long long id;
-      arr = unpinned_at(h, f, base + taken, &id);
+      arr = unpinned_at<H, BND>(h, f, base + taken, &id);
       taken++;
       h->cur[i] = id;
       rem = h->invr[i];
@@ -454,16 +457,16 @@ __device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
 }
 
 // returns the token grants of this step (same value in every lane)
-template <class H>
+template <class H, bool INTEG, bool BND>
 __device__ int hot_step(H* h, int lane, int w, int s) {
   const double t0 = (double)w * h->ws + (double)s * h->qs;
   const int n = h->n;
   const int F = h->F, G = h->G;
-  const bool integral = h->integral != 0;
+  constexpr bool integral = INTEG;
   // _admit_arrivals touches only queues and _complete_live_tokens only the
   // ledger, so admission runs first and completion fuses with the key pass.
 #pragma unroll 1
-  for (int f = lane; f < F; f += 32) hot_admit(h, f, t0);
+  for (int f = lane; f < F; f += 32) hot_admit<H, BND>(h, f, t0);
   if (s > 0 && !integral) hot_complete_sm(h, lane);
 #pragma unroll 1
   for (int g = lane; g < G; g += 32) {
@@ -624,7 +627,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       int avail = h->favail[f] - base;
       avail = avail < 0 ? 0 : (avail > picks ? picks : avail);
       int comp = 0, viol = 0;
-      serve_replay(h, i, f, t0, t_end, base, avail, comp, viol);
+      serve_replay<H, BND>(h, i, f, t0, t_end, base, avail, comp, viol);
       if (comp) atomicAdd(&h->fcomp[f], comp);
       if (viol) atomicAdd(&h->fviol[f], viol);
     }
@@ -650,7 +653,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     if (from_ns) {
       const int nsn = h->nsn[f] - from_ns;
       h->nsn[f] = nsn;
-      const int limit = h->maxq[f];
+      const int limit = BND ? h->maxq[f] : -1;
       if (limit >= 0) {
         h->rhead[f] = (h->rhead[f] + from_ns) % limit;
       } else if (nsn > 0) {
@@ -672,15 +675,28 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   return grants;
 }
 
-template <class H>
-__device__ __noinline__ long long hot_steps(H* h, int lane, int w) {
+// One instantiation per (integral SM partitions, any bounded queue): the
+// common case (integral, unbounded) carries neither the float dispatch nor
+// the bounded-queue ring code in its instruction stream.
+template <class H, bool INTEG, bool BND>
+__device__ __noinline__ long long hot_steps_t(H* h, int lane, int w) {
   const int T = h->T;
   long long grants = 0;
   #pragma unroll 1
-  for (int s = 0; s < T; s++) grants += hot_step(h, lane, w, s);
+  for (int s = 0; s < T; s++) grants += hot_step<H, INTEG, BND>(h, lane, w, s);
   hot_complete(h, lane);
   __syncwarp();
   return grants;
+}
+
+template <class H>
+__device__ long long hot_steps(H* h, int lane, int w) {
+  if (h->integral) {
+    return h->bounded ? hot_steps_t<H, true, true>(h, lane, w)
+                      : hot_steps_t<H, true, false>(h, lane, w);
+  }
+  return h->bounded ? hot_steps_t<H, false, true>(h, lane, w)
+                    : hot_steps_t<H, false, false>(h, lane, w);
 }
 
 // Window start when registration did not change (no epoch, nobody warmed

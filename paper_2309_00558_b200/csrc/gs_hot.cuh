@@ -25,6 +25,7 @@
 namespace gs {
 
 enum : int { GS_CAP_HOT = 5 };   // status detail: working set exceeds the size class
+constexpr double NOT_REQ = __builtin_huge_val();   // key of a pod that requests no token
 
 template <int PC_, int FC_, int GC_>
 struct Hot {
@@ -34,7 +35,9 @@ struct Hot {
   // (a granted pod's duration min(quantum, q_lim - q_used) is recomputed where
   // needed: q_used does not change between dispatch and completion)
   double qused[PC], qreq[PC], qlim[PC], sm[PC], busy[PC], crem[PC], carr[PC], invr[PC];
-  unsigned long long key[PC];
+  // build_queue key -(q_req - q_used) as a double (+inf: not requesting);
+  // double compares tie -0.0 with 0.0 exactly like Python's tuple order
+  double key[PC];
   long long cur[PC];
   int fnode[PC];
   // pod indices (PC <= 256) and flag bits (PF_CUR | PF_GRANT) fit in a byte
@@ -435,7 +438,7 @@ __device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
 #pragma unroll 1
       for (int j = h->seg[g]; j < e; j++) {
         const int i = h->order[j];
-        if (h->key[i] == ~0ull) break;          // rest of the node is not requesting
+        if (h->key[i] == NOT_REQ) break;          // rest of the node is not requesting
         const double sm = h->sm[i];
         if (sm + sr > SM_LIMIT + SM_EPS) break;
         const double rem = h->qlim[i] - h->qused[i];
@@ -490,7 +493,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     }
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
-    h->key[i] = req ? ord_key(-(h->qreq[i] - qused)) : ~0ull;
+    h->key[i] = req ? -(h->qreq[i] - qused) : NOT_REQ;
     if (req && integral) atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
     any_req |= req;
   }
@@ -508,31 +511,38 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
 #pragma unroll 1
   for (int i = lane; i < n; i += 32) {
     const int g = h->fnode[i] >> 16;
-    const unsigned long long k = h->key[i];
+    const double k = h->key[i];
     const int lo = h->seg[g], hi = h->seg[g + 1];
     int r = 0;
     // the SM sum ahead is only needed when the node's requesting SM can
     // exceed 100 (otherwise no requesting pod misfits)
-    const bool need_ahead = integral && k != ~0ull && h->reqsm[g] > (int)SM_LIMIT;
+    const bool need_ahead = integral && k != NOT_REQ && h->reqsm[g] > (int)SM_LIMIT;
     if (need_ahead) {
       double ahead = 0.0;
 #pragma unroll 1
       for (int j = lo; j < hi; j++) {
-        const unsigned long long kj = h->key[j];
+        const double kj = h->key[j];
         const bool less = (kj < k) || (kj == k && j < i);
         r += less;
         if (less) ahead += h->sm[j];
       }
       if (h->sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], r);
     } else {
+      // (key, pod index) order: pods before i count when key <= k, the rest
+      // when key < k; one convergent loop over the node for all its lanes
+      int j = lo;
 #pragma unroll 1
-      for (int j = lo; j < hi; j++) {
-        const unsigned long long kj = h->key[j];
-        r += (kj < k) || (kj == k && j < i);
+      for (; j + 1 < hi; j += 2) {
+        const double a = h->key[j], b = h->key[j + 1];
+        r += (int)(j < i ? a <= k : a < k) + (int)(j + 1 < i ? b <= k : b < k);
+      }
+      if (j < hi) {
+        const double a = h->key[j];
+        r += (int)(j < i ? a <= k : a < k);
       }
     }
     // (each order position is read and written only by the lane whose pod lands there)
-    if (integral && k != ~0ull && (int)h->order[lo + r] != i) atomicOr(&h->ostate[g], 1);
+    if (integral && k != NOT_REQ && (int)h->order[lo + r] != i) atomicOr(&h->ostate[g], 1);
     h->order[lo + r] = (unsigned char)i;
     h->rank[i] = (unsigned char)r;
   }
@@ -543,7 +553,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
 #pragma unroll 1
     for (int i = lane; i < n; i += 32) {
       const int g = h->fnode[i] >> 16;
-      if (h->key[i] != ~0ull && h->rank[i] < h->cut[g]) {
+      if (h->key[i] != NOT_REQ && h->rank[i] < h->cut[g]) {
         const double rem = h->qlim[i] - h->qused[i];
         const double dur = rem < quantum ? rem : quantum;
         h->flags[i] |= PF_GRANT;

@@ -37,24 +37,29 @@ __host__ __device__ inline Layout run_layout(const gs_scenario_t& sc, const gs_f
 }
 
 __device__ void init_run(Ctx& c) {
+  #pragma unroll 1
   for (int i = c.lane; i < c.P; i += 32) {
     c.t->p_flags[i] = 0;
     c.t->s_free[i] = c.P - 1 - i;  // slot 0 is allocated first
   }
+  #pragma unroll 1
   for (int f = c.lane; f < c.F; f += 32) {
     c.t->f_qlen[f] = 0; c.t->f_pinned[f] = 0; c.t->f_fw[f] = 0; c.t->f_fi[f] = 0; c.t->f_fn[f] = 0;
     c.t->f_nsn[f] = 0; c.t->f_nsw[f] = 0; c.t->f_nsi[f] = 0; c.t->f_rhead[f] = 0; c.t->f_retn[f] = 0;
     c.t->f_pctr[f] = 0; c.t->f_warr[f] = 0; c.t->f_wcomp[f] = 0; c.t->f_wviol[f] = 0; c.t->f_wdrop[f] = 0;
     c.t->f_hn[f] = 0;
   }
+  #pragma unroll 1
   for (int g = c.lane; g < c.G; g += 32) {
     c.t->n_sr[g] = 0.0; c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; c.t->n_fp[g] = 0.0;
     c.t->n_nfree[g] = 1; c.t->n_nres[g] = 0; c.t->n_nplaced[g] = 0;
     c.t->n_rect[g * c.R] = make_int4(0, 0, c.sc->side_x, c.sc->side_y);
   }
+  #pragma unroll 1
   for (int i = c.lane; i < c.G * c.F; i += 32) c.t->n_cnt[i] = 0;
   if (c.lane == 0) {
     int off = 0;
+    #pragma unroll 1
     for (int f = 0; f < c.F; f++) {
       c.t->f_ringoff[f] = off;
       if (c.fs[f].max_queue > 0) off += c.fs[f].max_queue;
@@ -71,6 +76,7 @@ __device__ void init_run(Ctx& c) {
 __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PySum& su,
                              PySum& so, int& peak, int& fail_total) {
   const gs_scenario_t& sc = *c.sc;
+  #pragma unroll 1
   for (int f = c.lane; f < c.F; f += 32) {
     int hn = c.t->f_hn[f];
     c.t->f_hist[3 * f + hn % 3] = (double)c.t->f_warr[f] / c.ws;   // history.append(n / W)
@@ -88,6 +94,7 @@ __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PyS
     c.t->f_wcomp[f] = 0; c.t->f_wviol[f] = 0; c.t->f_wdrop[f] = 0;
   }
   int in_use = 0;
+  #pragma unroll 1
   for (int g = c.lane; g < c.G; g += 32) {
     gs_gpu_row_t r;
     r.present = c.t->n_nplaced[g] > 0 ? 1 : 0;
@@ -102,6 +109,7 @@ __device__ void window_close(Ctx& c, int w, const gs_out_t& out, Accum& acc, PyS
   in_use = warp_sum_i(in_use);
   __syncwarp();
   if (c.lane == 0) {
+    #pragma unroll 1
     for (int g = 0; g < c.G; g++) {           // summary sums in CSV row order
       if (c.t->n_nplaced[g] <= 0) continue;
       double cov = c.t->n_cov[g], occ = c.t->n_occ[g];
@@ -127,6 +135,7 @@ template <class H>
 __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, PySum& su,
                           PySum& so, int& peak, int& fail_total) {
   const gs_scenario_t& sc = *c.sc;
+  #pragma unroll 1
   for (int f = c.lane; f < c.F; f += 32) {
     const int hn = h->hn[f];
     c.t->f_hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
@@ -144,6 +153,7 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
     h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
   }
   int in_use = 0;
+  #pragma unroll 1
   for (int g = c.lane; g < c.G; g += 32) {
     gs_gpu_row_t r;
     r.present = h->nplaced[g] > 0 ? 1 : 0;
@@ -158,6 +168,7 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
   in_use = warp_sum_i(in_use);
   __syncwarp();
   if (c.lane == 0) {
+    #pragma unroll 1
     for (int g = 0; g < c.G; g++) {           // summary sums in CSV row order
       if (h->nplaced[g] <= 0) continue;
       const double cov = h->cov[g], occ = h->occ[g];
@@ -222,8 +233,10 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   init_run(c);
   // initial pods: sorted fid order, spec order (sim_engine.py:436-441)
   if (c.lane == 0) {
+    #pragma unroll 1
     for (int f = 0; f < c.F && !c.sh->err; f++) {
       const gs_function_t& fs = c.fs[f];
+      #pragma unroll 1
       for (int i = 0; i < fs.n_init; i++) {
         const gs_init_t& ip = c.inits[fs.init_off + i];
         if (make_pod(c, f, ip.point, ip.has_q_req, ip.q_req, 0) < 0) break;
@@ -240,6 +253,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   if (!failed(c)) refresh_frag(c);
   bool hot_valid = false;
   long long pod_steps = 0, hot_grants = 0;   // hot-path counters kept in registers
+  #pragma unroll 1
   for (int w = 0; w < c.W && !failed(c); w++) {
     const bool epoch = w > 0 && w % c.sc->epoch_windows == 0;
     if constexpr (std::is_void<H>::value) {     // XL: working set stays in the HBM arena
@@ -248,8 +262,10 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
         if (failed(c)) break;
       }
       window_begin(c, w);
+      #pragma unroll 1
       for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
       __syncwarp();
+      #pragma unroll 1
       for (int s = 0; s < c.T; s++) run_step(c, w, s);
       complete_tokens(c);
       window_close(c, w, out, acc, su, so, peak, fail_total);
@@ -282,6 +298,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   memset(&st, 0, sizeof(st));
   int nplaced = 0;
   if (!c.sh->err) {
+    #pragma unroll 1
     for (int s0 = 0; s0 < c.P; s0 += 32) {
       int slot = s0 + c.lane;
       bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED);

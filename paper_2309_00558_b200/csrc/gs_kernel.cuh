@@ -72,9 +72,12 @@ __device__ __forceinline__ unsigned long long digits_key(int counter) {
   int d[10];
   int n = 0;
   unsigned v = (unsigned)counter;
+  #pragma unroll 1
   do { d[n++] = (int)(v % 10u); v /= 10u; } while (v && n < 10);
+  #pragma unroll 1
   while (n < 4) d[n++] = 0;
   unsigned long long key = 0;
+  #pragma unroll 1
   for (int i = 0; i < 10; i++) key = key * 11ull + (i < n ? (unsigned long long)(d[n - 1 - i] + 1) : 0ull);
   return key;
 }
@@ -246,8 +249,10 @@ __device__ void warp_sort(Ctx& c, int n) {
   unsigned long long* B = c.t->s_kd;
   int* V = c.t->s_ki;
   int q = 1;
+  #pragma unroll 1
   while (q < n) q <<= 1;
   if (q < 2) { __syncwarp(); return; }
+  #pragma unroll 1
   for (int i = n + c.lane; i < q; i += 32) { A[i] = ~0ull; B[i] = ~0ull; V[i] = 0x7fffffff; }
   __syncwarp();
   if (q <= 32) {
@@ -255,7 +260,9 @@ __device__ void warp_sort(Ctx& c, int n) {
     unsigned long long a = c.lane < q ? A[c.lane] : ~0ull;
     unsigned long long b = c.lane < q ? B[c.lane] : ~0ull;
     int v = c.lane < q ? V[c.lane] : 0x7fffffff;
+    #pragma unroll 1
     for (int k = 2; k <= q; k <<= 1) {
+      #pragma unroll 1
       for (int j = k >> 1; j > 0; j >>= 1) {
         unsigned long long oa = __shfl_xor_sync(FULL, a, j);
         unsigned long long ob = __shfl_xor_sync(FULL, b, j);
@@ -272,8 +279,11 @@ __device__ void warp_sort(Ctx& c, int n) {
     __syncwarp();
     return;
   }
+  #pragma unroll 1
   for (int k = 2; k <= q; k <<= 1) {
+    #pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
+      #pragma unroll 1
       for (int t = c.lane; t < (q >> 1); t += 32) {
         int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
         int l = i | j;
@@ -307,6 +317,7 @@ __device__ __forceinline__ double arrival_time(const Ctx& c, int f, int w, int i
 // advance (w, i) to the next generated request; caller guarantees one exists
 __device__ __forceinline__ void advance_id(const Ctx& c, int f, int& w, int& i) {
   i++;
+  #pragma unroll 1
   while (w < c.W && i >= c.count(f, w)) { w++; i = 0; }
 }
 
@@ -317,6 +328,7 @@ __device__ void refresh_footprint(Ctx& c, int g) {  // lane-agnostic, single lan
   double total = 0.0;
   int nres = c.t->n_nres[g];
   const bool sharing = (c.flags & GS_FLAG_SHARING) != 0;
+  #pragma unroll 1
   for (int i = 0; i < nres; i++) {
     int2 e = c.t->n_res[g * c.F + i];
     if (e.y <= 0) continue;
@@ -344,6 +356,7 @@ __device__ void mem_add(Ctx& c, int g, int f) {  // single lane
   int2* res = &c.t->n_res[g * c.F];
   if (*cnt > 0) {
     int n = c.t->n_nres[g];
+    #pragma unroll 1
     for (int i = 0; i < n; i++) if (res[i].x == f) { res[i].y++; break; }
   } else {
     res[c.t->n_nres[g]++] = make_int2(f, 1);
@@ -356,9 +369,11 @@ __device__ void mem_remove(Ctx& c, int g, int f) {  // single lane
   int* cnt = &c.t->n_cnt[g * c.F + f];
   int2* res = &c.t->n_res[g * c.F];
   int n = c.t->n_nres[g];
+  #pragma unroll 1
   for (int i = 0; i < n; i++) {
     if (res[i].x != f) continue;
     if (res[i].y == 1) {            // del resident[fid]: keep the order of the rest
+      #pragma unroll 1
       for (int j = i; j + 1 < n; j++) res[j] = res[j + 1];
       c.t->n_nres[g] = n - 1;
     } else {
@@ -391,6 +406,7 @@ __device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
   int n = *n_ptr;
   int4* tmp = c.t->s_carve;
   int base = 0;
+  #pragma unroll 1
   for (int s = 0; s < n; s += 32) {
     int j = s + c.lane;
     int4 parts[4];
@@ -410,6 +426,7 @@ __device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
     }
     int incl = warp_incl_scan(np, c.lane);
     int off = base + incl - np;
+    #pragma unroll 1
     for (int k = 0; k < np; k++) tmp[off + k] = parts[k];
     base += __shfl_sync(FULL, incl, 31);
   }
@@ -417,12 +434,14 @@ __device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
   int m = base;
   // prune: drop rects contained in another; exact duplicates keep the first
   int kept_base = 0;
+  #pragma unroll 1
   for (int s = 0; s < m; s += 32) {
     int i = s + c.lane;
     bool keep = false;
     if (i < m) {
       int4 r = tmp[i];
       keep = true;
+      #pragma unroll 1
       for (int j = 0; j < m; j++) {
         if (j == i) continue;
         int4 o = tmp[j];
@@ -438,6 +457,7 @@ __device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
   if (kept_base > cap) return false;
   // second pass writes (list may alias nothing in tmp)
   int outp = 0;
+  #pragma unroll 1
   for (int s = 0; s < m; s += 32) {
     int i = s + c.lane;
     bool keep = false;
@@ -445,6 +465,7 @@ __device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
     if (i < m) {
       r = tmp[i];
       keep = true;
+      #pragma unroll 1
       for (int j = 0; j < m; j++) {
         if (j == i) continue;
         int4 o = tmp[j];
@@ -502,10 +523,12 @@ __device__ int best_match(Ctx& c, int slot, int4* chosen) {
   BestKey best;
   best.idx = -1; best.k0 = 0; best.a = best.b = best.d = 0;
   long long scans = 0;
+  #pragma unroll 1
   for (int g = 0; g < c.G; g++) {
     if (!admit(c, g, f)) continue;
     int nf = c.t->n_nfree[g];
     scans += nf;
+    #pragma unroll 1
     for (int j = c.lane; j < nf; j += 32) {
       int4 r = c.t->n_rect[g * c.R + j];
       if (rw <= r.z && rh <= r.w) {
@@ -527,6 +550,7 @@ __device__ int best_fit_in_list(Ctx& c, const int4* list, int n, int w, int h) {
   long long area = (long long)w * h;
   BestKey best;
   best.idx = -1; best.k0 = 0; best.a = best.b = best.d = 0;
+  #pragma unroll 1
   for (int j = c.lane; j < n; j += 32) {
     int4 r = list[j];
     if (w <= r.z && h <= r.w) {
@@ -578,6 +602,7 @@ __device__ void return_request(Ctx& c, int f, long long id) {  // lane 0
   if (n >= c.RET) { set_error(c, GS_ERR_CAPACITY, GS_CAP_RETURNED, f, 0); return; }
   long long* r = &c.t->f_ret[(size_t)f * c.RET];
   int i = n;
+  #pragma unroll 1
   while (i > 0 && r[i - 1] > id) { r[i] = r[i - 1]; i--; }
   r[i] = id;
   c.t->f_retn[f] = n + 1;
@@ -630,6 +655,7 @@ __device__ bool place_pod(Ctx& c, int slot, int g, int4 chosen) {
 // (the retry list plus this epoch's additions); order (-area, pod_id).
 __device__ void place_batch(Ctx& c) {
   int nb = 0;
+  #pragma unroll 1
   for (int s = 0; s < c.P; s += 32) {
     int slot = s + c.lane;
     bool take = slot < c.P && (c.t->p_flags[slot] & (PF_ALIVE | PF_PLACED)) == PF_ALIVE;
@@ -647,6 +673,7 @@ __device__ void place_batch(Ctx& c) {
   __syncwarp();
   warp_sort(c, nb);
   // batch order + each entry's best_match inputs (function, w, h)
+  #pragma unroll 1
   for (int i = c.lane; i < nb; i += 32) {
     const int slot = c.t->s_ki[i];
     c.t->s_batch[i] = slot;
@@ -659,6 +686,7 @@ __device__ void place_batch(Ctx& c) {
   // too (nothing changes in between), so a whole run of them is settled at
   // once with the same counters (attempts, failures, rect scans, retry flag).
   int i = 0;
+  #pragma unroll 1
   while (i < nb) {
     const int slot = c.t->s_batch[i];
     int4 chosen;
@@ -675,12 +703,14 @@ __device__ void place_batch(Ctx& c) {
     const unsigned long long key_a = c.t->s_ka[i];
     const int key_f = c.t->s_ki[i];
     int j = nb;                                  // first later entry with another key
+    #pragma unroll 1
     for (int k0 = i + 1; k0 < nb; k0 += 32) {
       const int k = k0 + c.lane;
       const bool differs = k < nb && (c.t->s_ka[k] != key_a || c.t->s_ki[k] != key_f);
       const unsigned bal = __ballot_sync(FULL, differs);
       if (bal) { j = k0 + __ffs(bal) - 1; break; }
     }
+    #pragma unroll 1
     for (int k = i + c.lane; k < j; k += 32) c.t->p_flags[c.t->s_batch[k]] |= PF_RETRY;
     if (c.lane == 0) {
       const int len = j - i;
@@ -698,6 +728,7 @@ __device__ void place_batch(Ctx& c) {
 __device__ void restructure(Ctx& c, int g) {
   if (c.t->n_nfree[g] <= c.sc->restructure_threshold) return;
   int np = 0;
+  #pragma unroll 1
   for (int s = 0; s < c.P; s += 32) {
     int slot = s + c.lane;
     bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED) && c.t->p_node[slot] == g;
@@ -713,11 +744,13 @@ __device__ void restructure(Ctx& c, int g) {
   }
   __syncwarp();
   warp_sort(c, np);
+  #pragma unroll 1
   for (int i = c.lane; i < np; i += 32) c.t->s_list[i] = c.t->s_ki[i];
   int4* fr = c.t->s_rs;
   int* nfr = &c.sh->n_list;
   if (c.lane == 0) { fr[0] = make_int4(0, 0, c.sc->side_x, c.sc->side_y); *nfr = 1; }
   __syncwarp();
+  #pragma unroll 1
   for (int i = 0; i < np; i++) {
     int slot = c.t->s_list[i];
     int w = c.t->p_w[slot], h = c.t->p_h[slot];
@@ -736,7 +769,9 @@ __device__ void restructure(Ctx& c, int g) {
     __syncwarp();
   }
   int nn = *nfr;
+  #pragma unroll 1
   for (int j = c.lane; j < nn; j += 32) c.t->n_rect[g * c.R + j] = fr[j];
+  #pragma unroll 1
   for (int i = c.lane; i < np; i += 32) {
     int slot = c.t->s_list[i];
     c.t->p_x[slot] = c.t->s_pos[i].x;
@@ -749,8 +784,10 @@ __device__ void restructure(Ctx& c, int g) {
 // fragmentation index over all nodes' free rects (sim_engine.py:580-583)
 __device__ void refresh_frag(Ctx& c) {
   long long total = 0, largest = -1;
+  #pragma unroll 1
   for (int g = 0; g < c.G; g++) {
     int nf = c.t->n_nfree[g];
+    #pragma unroll 1
     for (int j = c.lane; j < nf; j += 32) {
       long long a = r_area(c.t->n_rect[g * c.R + j]);
       total += a;
@@ -772,8 +809,11 @@ __device__ void refresh_frag(Ctx& c) {
 __device__ __forceinline__ void warp_sort_regs(unsigned long long& a, unsigned long long& b,
                                                int& v, int n, int lane) {
   int q = 1;
+  #pragma unroll 1
   while (q < n) q <<= 1;
+  #pragma unroll 1
   for (int k = 2; k <= q; k <<= 1) {
+    #pragma unroll 1
     for (int j = k >> 1; j > 0; j >>= 1) {
       const unsigned long long oa = __shfl_xor_sync(FULL, a, j);
       const unsigned long long ob = __shfl_xor_sync(FULL, b, j);
@@ -792,8 +832,10 @@ __device__ __forceinline__ void warp_sort_regs(unsigned long long& a, unsigned l
 __device__ void group_alive_by_fn(Ctx& c) {
   int* off = c.t->f_loff;
   int* cur = c.t->s_fcur;
+  #pragma unroll 1
   for (int f = c.lane; f <= c.F; f += 32) cur[f] = 0;
   __syncwarp();
+  #pragma unroll 1
   for (int s0 = 0; s0 < c.P; s0 += 32) {
     const int slot = s0 + c.lane;
     const int fn = (slot < c.P && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
@@ -803,10 +845,12 @@ __device__ void group_alive_by_fn(Ctx& c) {
   __syncwarp();
   if (c.lane == 0) {                       // exclusive scan (F is small)
     int acc = 0;
+    #pragma unroll 1
     for (int f = 0; f < c.F; f++) { off[f] = acc; const int n = cur[f]; cur[f] = acc; acc += n; }
     off[c.F] = acc;
   }
   __syncwarp();
+  #pragma unroll 1
   for (int s0 = 0; s0 < c.P; s0 += 32) {
     const int slot = s0 + c.lane;
     const int fn = (slot < c.P && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
@@ -828,6 +872,7 @@ __device__ int ideal_point(const Ctx& c, int f, double residual) {
   const gs_function_t& fs = c.fs[f];
   double k0 = 0, k1 = 0, k2 = 0, k3 = 0;
   int idx = -1;
+  #pragma unroll 1
   for (int k = c.lane; k < fs.n_points; k += 32) {
     const gs_point_t& p = c.pt(f, k);
     if (!(p.thr > residual)) continue;
@@ -857,6 +902,7 @@ __device__ int ideal_point(const Ctx& c, int f, double residual) {
 // ----------------------------------------------------------------------------
 __device__ void run_epoch(Ctx& c, int w) {
   group_alive_by_fn(c);
+  #pragma unroll 1
   for (int f = 0; f < c.F; f++) {
     // running set of f: placed pods + retry pods (sim_engine.py:370-375),
     // ordered by (efficiency, pod_id) (autoscaler.py:50-51); T in that order
@@ -879,9 +925,11 @@ __device__ void run_epoch(Ctx& c, int w) {
         thr = c.pt(f, c.t->p_pt[v]).thr;
         c.t->s_ki[c.lane] = v;
       }
+      #pragma unroll 1
       for (int i = 0; i < n; i++) sup.add(__shfl_sync(FULL, thr, i));   // same in every lane
       __syncwarp();
     } else {
+      #pragma unroll 1
       for (int i = c.lane; i < n; i += 32) {
         const int slot = c.t->s_list[start + i];
         c.t->s_ka[i] = ord_key(c.pt(f, c.t->p_pt[slot]).rpr);
@@ -890,11 +938,13 @@ __device__ void run_epoch(Ctx& c, int w) {
       }
       __syncwarp();
       warp_sort(c, n);
+      #pragma unroll 1
       for (int i = 0; i < n; i++) sup.add(c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr);
     }
     const int hn = c.t->f_hn[f];
     const double* h = &c.t->f_hist[3 * f];
     double pred = h[(hn - 1) % 3];            // max(history[-3:])
+    #pragma unroll 1
     for (int k = 2; k <= 3 && k <= hn; k++) {
       const double x = h[(hn - k) % 3];
       if (x > pred) pred = x;
@@ -918,6 +968,7 @@ __device__ void run_epoch(Ctx& c, int w) {
         if (total > c.P) {
           set_error(c, GS_ERR_CAPACITY, GS_CAP_PODS, c.P, 1);
         } else {
+          #pragma unroll 1
           for (long long i = 0; i < total; i++) {
             const int k = i < cnt ? pe : ideal;
             if (make_pod(c, f, k, 0, 0.0, w + c.sc->cold_start_windows) < 0) break;
@@ -926,6 +977,7 @@ __device__ void run_epoch(Ctx& c, int w) {
       }
     } else if (gap < 0) {                     // scale_down: autoscaler.py:134-149
       double delta = gap;
+      #pragma unroll 1
       for (int i = 0; i < n && delta < 0; i++) {
         const double t = n <= 32 ? __shfl_sync(FULL, thr, i)
                                  : c.pt(f, c.t->p_pt[c.t->s_ki[i]]).thr;
@@ -942,6 +994,7 @@ __device__ void run_epoch(Ctx& c, int w) {
   }
   place_batch(c);
   if (failed(c)) return;
+  #pragma unroll 1
   for (int g = 0; g < c.G; g++) {
     restructure(c, g);
     if (failed(c)) return;
@@ -955,6 +1008,7 @@ __device__ void run_epoch(Ctx& c, int w) {
 // ----------------------------------------------------------------------------
 __device__ void window_begin(Ctx& c, int w) {
   int next_warm = 0x7fffffff;
+  #pragma unroll 1
   for (int slot = c.lane; slot < c.P; slot += 32) {
     int fl = c.t->p_flags[slot];
     if ((fl & PF_PLACED) && !(fl & PF_REG)) {
@@ -967,6 +1021,7 @@ __device__ void window_begin(Ctx& c, int w) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) next_warm = min(next_warm, __shfl_xor_sync(FULL, next_warm, o));
   if (c.lane == 0) c.sh->next_warm = next_warm;
+  #pragma unroll 1
   for (int f = c.lane; f < c.F; f += 32) {
     int n = c.count(f, w);
     c.t->f_warr[f] = n;
@@ -978,6 +1033,7 @@ __device__ void window_begin(Ctx& c, int w) {
   __syncwarp();
   // registered pods ordered by (node, pod_id)
   int nr = 0;
+  #pragma unroll 1
   for (int s = 0; s < c.P; s += 32) {
     int slot = s + c.lane;
     bool take = slot < c.P && (c.t->p_flags[slot] & PF_REG);
@@ -992,11 +1048,14 @@ __device__ void window_begin(Ctx& c, int w) {
   }
   __syncwarp();
   warp_sort(c, nr);
+  #pragma unroll 1
   for (int i = c.lane; i < nr; i += 32) c.t->s_rl[i] = c.t->s_ki[i];
   // node segments
+  #pragma unroll 1
   for (int g = c.lane; g <= c.G; g += 32) {
     // lower bound of node g in the sorted keys
     int lo = 0, hi = nr;
+    #pragma unroll 1
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
       if ((int)c.t->s_ka[mid] < g) lo = mid + 1; else hi = mid;
@@ -1007,12 +1066,14 @@ __device__ void window_begin(Ctx& c, int w) {
   // per-function lists in (node, pod_id) order: stable counting sort,
   // warp-parallel (match_any groups lanes of one function)
   int* cur = c.t->s_fcur;
+  #pragma unroll 1
   for (int f = c.lane; f <= c.F; f += 32) cur[f] = 0;
   if (c.lane == 0) {
     c.sh->n_reg = nr;
     c.sh->pod_steps += (long long)nr * c.T;
   }
   __syncwarp();
+  #pragma unroll 1
   for (int i0 = 0; i0 < nr; i0 += 32) {
     const int i = i0 + c.lane;
     const int fn = i < nr ? c.t->p_fn[c.t->s_rl[i]] : -1;
@@ -1022,10 +1083,12 @@ __device__ void window_begin(Ctx& c, int w) {
   __syncwarp();
   if (c.lane == 0) {
     int acc = 0;
+    #pragma unroll 1
     for (int f = 0; f < c.F; f++) { c.t->f_loff[f] = acc; const int k = cur[f]; cur[f] = acc; acc += k; }
     c.t->f_loff[c.F] = acc;
   }
   __syncwarp();
+  #pragma unroll 1
   for (int i0 = 0; i0 < nr; i0 += 32) {
     const int i = i0 + c.lane;
     const int slot = i < nr ? c.t->s_rl[i] : -1;
@@ -1045,8 +1108,10 @@ __device__ void complete_tokens(Ctx& c) {  // _complete_live_tokens (sim_engine.
   int n = c.sh->n_reg;
   if (!c.integral()) {
     // sm_running -= sm in token order per node, with the float-dust clamp
+    #pragma unroll 1
     for (int g = c.lane; g < c.G; g += 32) {
       double sr = c.t->n_sr[g];
+      #pragma unroll 1
       for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) {
         int slot = c.t->s_rl[c.t->s_ki[j]];
         if (!(c.t->p_flags[slot] & PF_GRANT)) break;
@@ -1057,6 +1122,7 @@ __device__ void complete_tokens(Ctx& c) {  // _complete_live_tokens (sim_engine.
     }
     __syncwarp();
   }
+  #pragma unroll 1
   for (int i = c.lane; i < n; i += 32) {
     int slot = c.t->s_rl[i];
     int fl = c.t->p_flags[slot];
@@ -1076,6 +1142,7 @@ __device__ void admit_arrivals(Ctx& c, int f, double t0) {  // sim_engine.py:472
   int qlen = c.t->f_qlen[f], nsn = c.t->f_nsn[f];
   int drop = 0;
   double now = t0 + TIME_EPS;
+  #pragma unroll 1
   while (fn > 0 && arrival_time(c, f, w, i) <= now) {
     int aw = w, ai = i;
     fn--;
@@ -1105,6 +1172,7 @@ __device__ void serve(Ctx& c, int slot, double t_start, double t_end) {
   double rem = c.t->p_crem[slot], arr = c.t->p_carr[slot];
   double slo = c.fs[f].slo_ms;
   int comp = 0, viol = 0;
+  #pragma unroll 1
   while (t < t_end - TIME_EPS) {
     if (!(fl & PF_CUR)) {
       long long id;
@@ -1113,6 +1181,7 @@ __device__ void serve(Ctx& c, int slot, double t_start, double t_end) {
       if (retn > 0) {
         long long* r = &c.t->f_ret[(size_t)f * c.RET];
         id = r[0];
+        #pragma unroll 1
         for (int k = 1; k < retn; k++) r[k - 1] = r[k];
         c.t->f_retn[f] = retn - 1;
       } else if (nsn > 0) {
@@ -1160,10 +1229,12 @@ __device__ void serve(Ctx& c, int slot, double t_start, double t_end) {
 __device__ void run_step(Ctx& c, int w, int s) {
   const double t0 = (double)w * c.ws + (double)s * c.qs;
   if (s > 0) complete_tokens(c);   // step 0: window_begin already reset the ledger
+  #pragma unroll 1
   for (int f = c.lane; f < c.F; f += 32) admit_arrivals(c, f, t0);
   __syncwarp();
   // filter_pods + requesting + build_queue keys
   const int n = c.sh->n_reg;
+  #pragma unroll 1
   for (int i = c.lane; i < n; i += 32) {
     int slot = c.t->s_rl[i];
     int fl = c.t->p_flags[slot];
@@ -1179,12 +1250,14 @@ __device__ void run_step(Ctx& c, int w, int s) {
   warp_sort(c, n);
   // dispatch (head-blocking) + coverage/occupancy, one lane per node
   int grants = 0;
+  #pragma unroll 1
   for (int g = c.lane; g < c.G; g += 32) {
     double sr = c.integral() ? 0.0 : c.t->n_sr[g];
     double mx = 0.0;
     PySum occ;
     occ.reset();
     int ng = 0;
+    #pragma unroll 1
     for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) {
       if (c.t->s_ka[j] & 1ull) break;           // rest of the node is not requesting
       int slot = c.t->s_rl[c.t->s_ki[j]];
@@ -1210,7 +1283,9 @@ __device__ void run_step(Ctx& c, int w, int s) {
   if (c.lane == 0) c.sh->grants += grants;
   __syncwarp();
   // serve, per function in (node, pod_id) order
+  #pragma unroll 1
   for (int f = c.lane; f < c.F; f += 32) {
+    #pragma unroll 1
     for (int j = c.t->f_loff[f]; j < c.t->f_loff[f + 1]; j++) {
       int slot = c.t->s_fl[j];
       if (c.t->p_flags[slot] & PF_GRANT) serve(c, slot, t0, t0 + c.t->p_dur[slot] * c.ws);

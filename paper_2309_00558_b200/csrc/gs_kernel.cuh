@@ -83,7 +83,7 @@ __device__ __forceinline__ unsigned long long digits_key(int counter) {
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
-#pragma unroll
+#pragma unroll 1
   for (int o = 1; o < 32; o <<= 1) {
     int y = __shfl_up_sync(FULL, v, o);
     if (lane >= o) v += y;
@@ -97,12 +97,12 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
-#pragma unroll
+#pragma unroll 1
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
 __device__ __forceinline__ long long warp_max_ll(long long v) {
-#pragma unroll
+#pragma unroll 1
   for (int o = 16; o > 0; o >>= 1) {
     long long y = __shfl_xor_sync(FULL, v, o);
     v = y > v ? y : v;
@@ -244,7 +244,7 @@ __device__ __forceinline__ bool trip_less(unsigned long long a1, unsigned long l
   return a1 < a2 || (a1 == a2 && (b1 < b2 || (b1 == b2 && v1 < v2)));
 }
 
-__device__ void warp_sort(Ctx& c, int n) {
+__device__ __noinline__ void warp_sort(Ctx& c, int n) {
   unsigned long long* A = c.t->s_ka;
   unsigned long long* B = c.t->s_kd;
   int* V = c.t->s_ki;
@@ -402,7 +402,7 @@ __device__ __forceinline__ long long r_area(int4 r) { return (long long)r.z * (l
 // _carve + _subdivide + _prune_contained (packer.py:196-242) on `list[0..*n)`,
 // warp-cooperative, stable.  Returns false (and leaves the list untouched)
 // when the pruned result would exceed `cap`.
-__device__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
+__device__ __noinline__ bool carve(Ctx& c, int4* list, int* n_ptr, int4 placed, int cap) {
   int n = *n_ptr;
   int4* tmp = c.t->s_carve;
   int base = 0;
@@ -501,7 +501,7 @@ __device__ __forceinline__ bool bk_less(const BestKey& x, const BestKey& y) {
   return x.idx < y.idx;
 }
 __device__ BestKey warp_argmin(BestKey k) {
-#pragma unroll
+#pragma unroll 1
   for (int o = 16; o > 0; o >>= 1) {
     BestKey y;
     y.k0 = __shfl_xor_sync(FULL, k.k0, o);
@@ -516,7 +516,7 @@ __device__ BestKey warp_argmin(BestKey k) {
 
 // best_match (packer.py:169-193): key (r.area - req.area, gpu, y, x), first
 // in (gpu, list) order on full ties.  Returns node (or -1) and the rect.
-__device__ int best_match(Ctx& c, int slot, int4* chosen) {
+__device__ __noinline__ int best_match(Ctx& c, int slot, int4* chosen) {
   int f = c.t->p_fn[slot];
   int rw = c.t->p_w[slot], rh = c.t->p_h[slot];
   long long rarea = (long long)rw * rh;
@@ -546,7 +546,7 @@ __device__ int best_match(Ctx& c, int slot, int4* chosen) {
 }
 
 // _best_fit_in_node (packer.py:278-287) on an arbitrary list
-__device__ int best_fit_in_list(Ctx& c, const int4* list, int n, int w, int h) {
+__device__ __noinline__ int best_fit_in_list(Ctx& c, const int4* list, int n, int w, int h) {
   long long area = (long long)w * h;
   BestKey best;
   best.idx = -1; best.k0 = 0; best.a = best.b = best.d = 0;
@@ -882,7 +882,7 @@ __device__ int ideal_point(const Ctx& c, int f, double residual) {
       k0 = d; k1 = p.area; k2 = p.sm; k3 = p.quota; idx = k;
     }
   }
-#pragma unroll
+#pragma unroll 1
   for (int o = 16; o > 0; o >>= 1) {
     const double y0 = __shfl_xor_sync(FULL, k0, o), y1 = __shfl_xor_sync(FULL, k1, o);
     const double y2 = __shfl_xor_sync(FULL, k2, o), y3 = __shfl_xor_sync(FULL, k3, o);

@@ -15,6 +15,7 @@
 #include "gs_kernel.cuh"
 #include "gs_hot.cuh"
 #include "gs_audit.cuh"
+#include "gs_xl.cuh"
 
 namespace gs {
 
@@ -228,6 +229,65 @@ __device__ void copy_out_run(const gs_scenario_t& sc, const gs_out_t& out, const
                sizeof(gs_placement_t) * (size_t)nplaced, lane);
 }
 
+// status, summary, final placements and the zero-copy row copy-out of a
+// finished run (warp-level; lane 0 writes the records)
+__device__ void finish_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run,
+                           Accum& acc, PySum& su, PySum& so, int peak, int fail_total,
+                           long long hot_grants, long long hot_pod_steps, int cls,
+                           bool hot_counters) {
+  // outputs
+  gs_status_t st;
+  memset(&st, 0, sizeof(st));
+  int nplaced = 0;
+  if (!c.sh->err) {
+    #pragma unroll 1
+    for (int s0 = 0; s0 < c.P; s0 += 32) {
+      int slot = s0 + c.lane;
+      bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED);
+      unsigned bal = __ballot_sync(FULL, take);
+      if (take && out.placements) {
+        int k = nplaced + __popc(bal & ((1u << c.lane) - 1u));
+        gs_placement_t p;
+        p.node = c.t->p_node[slot]; p.func = c.t->p_fn[slot]; p.counter = c.t->p_ctr[slot];
+        p.x = c.t->p_x[slot]; p.y = c.t->p_y[slot]; p.w = c.t->p_w[slot]; p.h = c.t->p_h[slot]; p.pad = 0;
+        out.placements[c.sc->place_off + k] = p;
+      }
+      nplaced += __popc(bal);
+    }
+  }
+  acc.arrivals = warp_sum_ll(acc.arrivals);
+  acc.completions = warp_sum_ll(acc.completions);
+  acc.violations = warp_sum_ll(acc.violations);
+  acc.dropped = warp_sum_ll(acc.dropped);
+  acc.final_depth = warp_sum_ll(acc.final_depth);
+  __syncwarp();
+  if (c.lane == 0) {
+    st.code = c.sh->err; st.detail = c.sh->err_detail;
+    st.arg0 = c.sh->err_a0; st.arg1 = c.sh->err_a1;
+    st.n_placements = nplaced;
+    st.hot_class = cls;
+    st.token_grants = c.sh->grants + hot_grants;
+    st.scale_decisions = c.sh->decisions;
+    st.placement_attempts = c.sh->attempts;
+    st.pod_steps = hot_counters ? hot_pod_steps : c.sh->pod_steps;
+    st.rect_scans = c.sh->rect_scans;
+    st.peak_pods = c.P - c.sh->min_free;
+    out.status[run] = st;
+    if (out.summary) {
+      gs_summary_t sm;
+      sm.windows = c.W; sm.gpus_used_peak = peak; sm.placement_failures = fail_total;
+      sm.n_gpu_rows = su.n;
+      sm.arrivals = acc.arrivals; sm.completions = acc.completions;
+      sm.slo_violations = acc.violations; sm.dropped = acc.dropped;
+      sm.final_queue_depth = acc.final_depth;
+      sm.sum_utilization = su.value(); sm.sum_sm_occupancy = so.value();
+      out.summary[run] = sm;
+    }
+  }
+  __syncwarp();
+  if (!c.sh->err) copy_out_run(*c.sc, out, host, nplaced, c.lane);
+}
+
 template <class H>
 __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run, H* h) {
   init_run(c);
@@ -293,57 +353,66 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   if constexpr (!std::is_void<H>::value) {
     if (hot_valid && !c.sh->err) hot_store(c, h);   // flush the last windows' counters
   }
-  // outputs
-  gs_status_t st;
-  memset(&st, 0, sizeof(st));
-  int nplaced = 0;
-  if (!c.sh->err) {
-    #pragma unroll 1
-    for (int s0 = 0; s0 < c.P; s0 += 32) {
-      int slot = s0 + c.lane;
-      bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED);
-      unsigned bal = __ballot_sync(FULL, take);
-      if (take && out.placements) {
-        int k = nplaced + __popc(bal & ((1u << c.lane) - 1u));
-        gs_placement_t p;
-        p.node = c.t->p_node[slot]; p.func = c.t->p_fn[slot]; p.counter = c.t->p_ctr[slot];
-        p.x = c.t->p_x[slot]; p.y = c.t->p_y[slot]; p.w = c.t->p_w[slot]; p.h = c.t->p_h[slot]; p.pad = 0;
-        out.placements[c.sc->place_off + k] = p;
+  finish_run(c, out, host, run, acc, su, so, peak, fail_total, hot_grants, pod_steps,
+             class_id<H>(), !std::is_void<H>::value);
+}
+
+
+// XL class driver: warp 0 runs the control code (as simulate_run<void>), all
+// XL_THREADS threads run the quantum steps (gs_xl.cuh).  Every thread calls
+// this with its own Ctx view of the same run.
+__device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run,
+                                XlShared* xs) {
+  const bool w0 = threadIdx.x < 32;
+  Accum acc = {0, 0, 0, 0, 0};
+  PySum su, so;
+  su.reset();
+  so.reset();
+  int peak = 0, fail_total = 0;
+  if (w0) {
+    init_run(c);
+    if (c.lane == 0) {
+      #pragma unroll 1
+      for (int f = 0; f < c.F && !c.sh->err; f++) {
+        const gs_function_t& fs = c.fs[f];
+        #pragma unroll 1
+        for (int i = 0; i < fs.n_init; i++) {
+          const gs_init_t& ip = c.inits[fs.init_off + i];
+          if (make_pod(c, f, ip.point, ip.has_q_req, ip.q_req, 0) < 0) break;
+        }
       }
-      nplaced += __popc(bal);
     }
+    __syncwarp();
+    if (!failed(c)) place_batch(c);
+    if (!failed(c)) refresh_frag(c);
   }
-  acc.arrivals = warp_sum_ll(acc.arrivals);
-  acc.completions = warp_sum_ll(acc.completions);
-  acc.violations = warp_sum_ll(acc.violations);
-  acc.dropped = warp_sum_ll(acc.dropped);
-  acc.final_depth = warp_sum_ll(acc.final_depth);
-  __syncwarp();
-  if (c.lane == 0) {
-    st.code = c.sh->err; st.detail = c.sh->err_detail;
-    st.arg0 = c.sh->err_a0; st.arg1 = c.sh->err_a1;
-    st.n_placements = nplaced;
-    st.hot_class = class_id<H>();
-    st.token_grants = c.sh->grants + hot_grants;
-    st.scale_decisions = c.sh->decisions;
-    st.placement_attempts = c.sh->attempts;
-    st.pod_steps = std::is_void<H>::value ? c.sh->pod_steps : pod_steps;
-    st.rect_scans = c.sh->rect_scans;
-    st.peak_pods = c.P - c.sh->min_free;
-    out.status[run] = st;
-    if (out.summary) {
-      gs_summary_t sm;
-      sm.windows = c.W; sm.gpus_used_peak = peak; sm.placement_failures = fail_total;
-      sm.n_gpu_rows = su.n;
-      sm.arrivals = acc.arrivals; sm.completions = acc.completions;
-      sm.slo_violations = acc.violations; sm.dropped = acc.dropped;
-      sm.final_queue_depth = acc.final_depth;
-      sm.sum_utilization = su.value(); sm.sum_sm_occupancy = so.value();
-      out.summary[run] = sm;
+  __syncthreads();
+  #pragma unroll 1
+  for (int w = 0; w < c.W; w++) {
+    if (w0) {
+      bool stop = failed(c);
+      if (!stop && w > 0 && w % c.sc->epoch_windows == 0) {
+        run_epoch(c, w);
+        stop = failed(c);
+      }
+      if (!stop) {
+        window_begin(c, w);
+        #pragma unroll 1
+        for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
+      }
+      __syncwarp();
+      if (c.lane == 0) xs->stop = stop ? 1 : 0;
     }
+    __syncthreads();
+    if (xs->stop) break;
+    #pragma unroll 1
+    for (int s = 0; s < c.T; s++) xl_step(c, w, s, xs);
+    xl_complete(c);
+    if (w0) window_close(c, w, out, acc, su, so, peak, fail_total);
+    __syncthreads();
   }
-  __syncwarp();
-  if (!c.sh->err) copy_out_run(*c.sc, out, host, nplaced, c.lane);
+  if (w0) finish_run(c, out, host, run, acc, su, so, peak, fail_total, 0, 0, 4, false);
+  __syncthreads();
 }
 
 struct KArgs {
@@ -391,6 +460,43 @@ gs_sim_kernel(KArgs a) {
     Layout L = run_layout(*c.sc, c.fs);
     ctx_bind(c, a.arena + a.ws_off[run], L);
     simulate_run<H>(c, a.out, a.host, run, hot);
+  }
+}
+
+
+// XL class: one run per CTA of XL_THREADS threads, runs pulled from the work
+// counter longest first.
+__global__ void __launch_bounds__(XL_THREADS, 1) gs_sim_kernel_xl(KArgs a) {
+  __shared__ WarpShared sh;
+  __shared__ XlShared xs;
+  for (;;) {
+    if (threadIdx.x == 0) xs.run = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int r = xs.run;
+    __syncthreads();
+    if (r >= a.n_order) break;
+    const int run = a.order[r];
+    Ctx c;
+    c.sc = &a.in.runs[run];
+    c.fs = &a.in.funcs[c.sc->func_off];
+    c.points = a.in.points;
+    c.counts = a.in.counts;
+    c.inits = a.in.inits;
+    c.G = c.sc->n_nodes; c.F = c.sc->n_funcs; c.P = c.sc->cap_pods; c.R = c.sc->cap_rects;
+    c.RET = c.sc->cap_returned; c.W = c.sc->windows; c.T = c.sc->steps; c.flags = c.sc->flags;
+    c.ws = c.sc->window_s; c.qs = c.sc->quantum_s; c.quantum = c.sc->quantum;
+    c.cap_mb = c.sc->capacity_mb;
+    c.lane = threadIdx.x & 31;
+    c.sh = &sh;
+    c.t = &sh.tab;
+    if (threadIdx.x < 32) {
+      Layout L = run_layout(*c.sc, c.fs);
+      ctx_bind(c, a.arena + a.ws_off[run], L);
+    } else {
+      c.Q = 0;
+    }
+    __syncthreads();
+    simulate_run_xl(c, a.out, a.host, run, &xs);
   }
 }
 
@@ -610,6 +716,14 @@ static int launch_class(const KArgs& a, int sms, cudaStream_t st, char* err, siz
   return GS_OK;
 }
 
+static int launch_xl(const KArgs& a, int sms, cudaStream_t st, char* err, size_t err_len) {
+  long long blocks = sms;
+  if (a.n_order < blocks) blocks = a.n_order > 0 ? a.n_order : 1;
+  gs_sim_kernel_xl<<<(unsigned)blocks, XL_THREADS, 0, st>>>(a);
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
 extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size_t err_len) {
   if (!s) { put_err(err, err_len, "null session"); return GS_ERR_ARG; }
   CK(cudaSetDevice(s->device));
@@ -636,7 +750,7 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
       case 1: rc = launch_class<HotS>(a, sms, st, err, err_len); break;
       case 2: rc = launch_class<HotM>(a, sms, st, err, err_len); break;
       case 3: rc = launch_class<HotL>(a, sms, st, err, err_len); break;
-      default: rc = launch_class<void>(a, sms, st, err, err_len); break;
+      default: rc = launch_xl(a, sms, st, err, err_len); break;
     }
     if (rc != GS_OK) return rc;
     s->last_launches++;

@@ -133,6 +133,8 @@ struct CtxTab {
   int4* n_rect;
   int2* n_res;
   int* n_cnt;
+  int *n_reqsm, *n_cut, *n_ngr;
+  unsigned long long* n_covb;
   // scratch
   int *s_rl, *s_fl, *s_free, *s_batch, *s_list;
   unsigned long long *s_ka, *s_kd;
@@ -210,6 +212,9 @@ __device__ void ctx_bind(Ctx& c, char* base, const Layout& L) {  // lane 0 write
   t.n_rect = carve_ptr<int4>(base, L.n_rect);
   t.n_res = carve_ptr<int2>(base, L.n_res);
   t.n_cnt = carve_ptr<int>(base, L.n_cnt);
+  t.n_reqsm = carve_ptr<int>(base, L.n_reqsm); t.n_cut = carve_ptr<int>(base, L.n_cut);
+  t.n_ngr = carve_ptr<int>(base, L.n_ngr);
+  t.n_covb = carve_ptr<unsigned long long>(base, L.n_covb);
   t.s_rl = carve_ptr<int>(base, L.s_rl); t.s_fl = carve_ptr<int>(base, L.s_fl);
   t.s_free = carve_ptr<int>(base, L.s_free); t.s_batch = carve_ptr<int>(base, L.s_batch);
   t.s_list = carve_ptr<int>(base, L.s_list);

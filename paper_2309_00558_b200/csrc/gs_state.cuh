@@ -40,6 +40,8 @@ struct Layout {
   size_t n_rect;                                       // int4 [G*R]
   size_t n_res;                                        // int2 [G*F] resident (fn,count), insertion order
   size_t n_cnt;                                        // i32 [G*F] dense resident counts
+  size_t n_reqsm, n_cut, n_ngr;                        // i32 [G] XL step scratch
+  size_t n_covb;                                       // u64 [G] XL step scratch
   // scratch
   size_t s_rl, s_fl, s_free, s_batch, s_list;         // i32 [P]
   size_t s_ka;                                         // u64 [Q]  Q = pow2 >= P
@@ -91,6 +93,8 @@ __host__ __device__ inline Layout gs_make_layout(int G, int F, int P, int R, int
   take(L.n_rect, (size_t)G * R, 16);
   take(L.n_res, (size_t)G * F, 8);
   take(L.n_cnt, (size_t)G * F, I);
+  take(L.n_reqsm, G, I); take(L.n_cut, G, I); take(L.n_ngr, G, I);
+  take(L.n_covb, G, D);
   int Q = gs_pow2_at_least(P > 32 ? P : 32);
   L.Q = Q;
   take(L.s_rl, P, I); take(L.s_fl, P, I); take(L.s_free, P, I);

@@ -240,10 +240,11 @@ __device__ void finish_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, in
   memset(&st, 0, sizeof(st));
   int nplaced = 0;
   if (!c.sh->err) {
+    const int phi = pod_high(c);
     #pragma unroll 1
-    for (int s0 = 0; s0 < c.P; s0 += 32) {
+    for (int s0 = 0; s0 < phi; s0 += 32) {
       int slot = s0 + c.lane;
-      bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED);
+      bool take = slot < phi && (c.t->p_flags[slot] & PF_PLACED);
       unsigned bal = __ballot_sync(FULL, take);
       if (take && out.placements) {
         int k = nplaced + __popc(bal & ((1u << c.lane) - 1u));
@@ -387,22 +388,32 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
     if (!failed(c)) refresh_frag(c);
   }
   __syncthreads();
+  bool lists_valid = false;            // s_rl / n_seg / s_fl match the registered set
   #pragma unroll 1
   for (int w = 0; w < c.W; w++) {
-    if (w0) {
-      bool stop = failed(c);
-      if (!stop && w > 0 && w % c.sc->epoch_windows == 0) {
-        run_epoch(c, w);
-        stop = failed(c);
+    // registration changes only at epochs and warm-ups; otherwise the sorted
+    // registered list and the per-function lists carry over (cf. hot_begin_light)
+    const bool epoch = w > 0 && w % c.sc->epoch_windows == 0;
+    const bool rebuild = !lists_valid || epoch || w >= c.sh->next_warm;
+    __syncthreads();                   // everyone read next_warm before warp 0 moves on
+    if (rebuild) {
+      if (w0) {
+        bool stop = failed(c);
+        if (!stop && epoch) {
+          run_epoch(c, w);
+          stop = failed(c);
+        }
+        if (!stop) window_begin(c, w);
+        __syncwarp();
+        if (c.lane == 0) xs->stop = stop ? 1 : 0;
       }
-      if (!stop) {
-        window_begin(c, w);
-        #pragma unroll 1
-        for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
-      }
-      __syncwarp();
-      if (c.lane == 0) xs->stop = stop ? 1 : 0;
+      lists_valid = true;
+    } else {
+      xl_begin_light(c, w);
+      if (threadIdx.x == 0) xs->stop = 0;
     }
+    #pragma unroll 1
+    for (int g = threadIdx.x; g < c.G; g += blockDim.x) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
     __syncthreads();
     if (xs->stop) break;
     #pragma unroll 1

@@ -230,6 +230,11 @@ __device__ void ctx_bind(Ctx& c, char* base, const Layout& L) {  // lane 0 write
   c.Q = L.Q;
 }
 
+// Pod slots ever allocated are exactly [0, P - min_free): the free stack hands
+// out fresh slots in increasing order and reuses freed ones first, so every
+// scan over pods can stop at this high-water mark instead of the capacity.
+__device__ __forceinline__ int pod_high(const Ctx& c) { return c.P - c.sh->min_free; }
+
 __device__ __forceinline__ void set_error(Ctx& c, int code, int detail, int a0, int a1) {
   // lane-agnostic: first error wins
   if (c.sh->err == 0) {
@@ -660,10 +665,11 @@ __device__ bool place_pod(Ctx& c, int slot, int g, int4 chosen) {
 // (the retry list plus this epoch's additions); order (-area, pod_id).
 __device__ void place_batch(Ctx& c) {
   int nb = 0;
+  const int phi = pod_high(c);
   #pragma unroll 1
-  for (int s = 0; s < c.P; s += 32) {
+  for (int s = 0; s < phi; s += 32) {
     int slot = s + c.lane;
-    bool take = slot < c.P && (c.t->p_flags[slot] & (PF_ALIVE | PF_PLACED)) == PF_ALIVE;
+    bool take = slot < phi && (c.t->p_flags[slot] & (PF_ALIVE | PF_PLACED)) == PF_ALIVE;
     unsigned bal = __ballot_sync(FULL, take);
     if (take) {
       int i = nb + __popc(bal & ((1u << c.lane) - 1u));
@@ -733,10 +739,11 @@ __device__ void place_batch(Ctx& c) {
 __device__ void restructure(Ctx& c, int g) {
   if (c.t->n_nfree[g] <= c.sc->restructure_threshold) return;
   int np = 0;
+  const int phi = pod_high(c);
   #pragma unroll 1
-  for (int s = 0; s < c.P; s += 32) {
+  for (int s = 0; s < phi; s += 32) {
     int slot = s + c.lane;
-    bool take = slot < c.P && (c.t->p_flags[slot] & PF_PLACED) && c.t->p_node[slot] == g;
+    bool take = slot < phi && (c.t->p_flags[slot] & PF_PLACED) && c.t->p_node[slot] == g;
     unsigned bal = __ballot_sync(FULL, take);
     if (take) {
       int i = np + __popc(bal & ((1u << c.lane) - 1u));
@@ -835,15 +842,16 @@ __device__ __forceinline__ void warp_sort_regs(unsigned long long& a, unsigned l
 // alive pods grouped by function, slot order inside a group:
 // s_list[f_loff[f] .. f_loff[f+1]).  (f_loff is scratch until window_begin.)
 __device__ void group_alive_by_fn(Ctx& c) {
+  const int phi = pod_high(c);
   int* off = c.t->f_loff;
   int* cur = c.t->s_fcur;
   #pragma unroll 1
   for (int f = c.lane; f <= c.F; f += 32) cur[f] = 0;
   __syncwarp();
   #pragma unroll 1
-  for (int s0 = 0; s0 < c.P; s0 += 32) {
+  for (int s0 = 0; s0 < phi; s0 += 32) {
     const int slot = s0 + c.lane;
-    const int fn = (slot < c.P && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
+    const int fn = (slot < phi && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
     const unsigned m = __match_any_sync(FULL, fn);
     if (fn >= 0 && c.lane == __ffs(m) - 1) atomicAdd(&cur[fn], __popc(m));
   }
@@ -856,9 +864,9 @@ __device__ void group_alive_by_fn(Ctx& c) {
   }
   __syncwarp();
   #pragma unroll 1
-  for (int s0 = 0; s0 < c.P; s0 += 32) {
+  for (int s0 = 0; s0 < phi; s0 += 32) {
     const int slot = s0 + c.lane;
-    const int fn = (slot < c.P && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
+    const int fn = (slot < phi && (c.t->p_flags[slot] & PF_ALIVE)) ? c.t->p_fn[slot] : -1;
     const unsigned m = __match_any_sync(FULL, fn);
     if (fn >= 0) {
       const int pos = cur[fn] + __popc(m & ((1u << c.lane) - 1u));
@@ -1013,8 +1021,9 @@ __device__ void run_epoch(Ctx& c, int w) {
 // ----------------------------------------------------------------------------
 __device__ void window_begin(Ctx& c, int w) {
   int next_warm = 0x7fffffff;
+  const int phi = pod_high(c);
   #pragma unroll 1
-  for (int slot = c.lane; slot < c.P; slot += 32) {
+  for (int slot = c.lane; slot < phi; slot += 32) {
     int fl = c.t->p_flags[slot];
     if ((fl & PF_PLACED) && !(fl & PF_REG)) {
       if (c.t->p_warm[slot] <= w) fl |= PF_REG;
@@ -1039,9 +1048,9 @@ __device__ void window_begin(Ctx& c, int w) {
   // registered pods ordered by (node, pod_id)
   int nr = 0;
   #pragma unroll 1
-  for (int s = 0; s < c.P; s += 32) {
+  for (int s = 0; s < phi; s += 32) {
     int slot = s + c.lane;
-    bool take = slot < c.P && (c.t->p_flags[slot] & PF_REG);
+    bool take = slot < phi && (c.t->p_flags[slot] & PF_REG);
     unsigned bal = __ballot_sync(FULL, take);
     if (take) {
       int i = nr + __popc(bal & ((1u << c.lane) - 1u));

@@ -70,6 +70,29 @@ __device__ void xl_complete(Ctx& c) {
   __syncthreads();
 }
 
+// window start with an unchanged registered set (no epoch, no warm-up):
+// reset_window + _generate_arrivals, CTA-wide (sim_engine.py:446-449)
+__device__ void xl_begin_light(Ctx& c, int w) {
+  const int n = c.sh->n_reg;
+  const int* rl = c.t->s_rl;
+#pragma unroll 1
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int slot = rl[i];
+    c.t->p_qused[slot] = 0.0;
+    c.t->p_flags[slot] &= ~PF_GRANT;
+  }
+#pragma unroll 1
+  for (int f = threadIdx.x; f < c.F; f += blockDim.x) {
+    const int k = c.count(f, w);
+    c.t->f_warr[f] = k;
+    if (k > 0) {
+      if (c.t->f_fn[f] == 0) { c.t->f_fw[f] = w; c.t->f_fi[f] = 0; }
+      c.t->f_fn[f] += k;
+    }
+  }
+  if (threadIdx.x == 0) c.sh->pod_steps += (long long)n * c.T;
+}
+
 // one quantum step (sim_engine.py:493-520) on every thread of the CTA
 __device__ void xl_step(Ctx& c, int w, int s, XlShared* xs) {
   const double t0 = (double)w * c.ws + (double)s * c.qs;

@@ -24,7 +24,7 @@ subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capt
 cub = glob.glob(tmp + "/*.cubin")[0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
 secs = re.split(r"\n\s*\.section\s+\.text\.", dis)
-dis = [s for s in secs if s.startswith("_ZN2gs13gs_sim_kernel") and kname in s.split(",")[0]][0]
+dis = [s for s in secs if s.startswith("_ZN2gs") and "gs_sim_kernel" in s.split(",")[0] and kname in s.split(",")[0]][0]
 line_of, cur = {}, None
 for l in dis.splitlines():
     m = re.match(r'\s*//## File "([^"]+)", line (\d+)', l)

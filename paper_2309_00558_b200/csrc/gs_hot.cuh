@@ -26,6 +26,7 @@ namespace gs {
 
 enum : int { GS_CAP_HOT = 5 };   // status detail: working set exceeds the size class
 constexpr double NOT_REQ = __builtin_huge_val();   // key of a pod that requests no token
+constexpr unsigned long long FULL_Q = ~0ull;        // covbits: some token had the full quantum
 
 template <int PC_, int FC_, int GC_>
 struct Hot {
@@ -60,6 +61,7 @@ struct Hot {
   // per step: requesting SM (integral), grants, 1 = dispatch order changed /
   // 2 = a partial token; occupancy-sum cache of the last all-quantum step
   int reqsm[GC], ngr[GC], ostate[GC], occn[GC];
+  int maycut[GC];                  // registered SM on the node can exceed 100 (per hot set)
   double occv[GC];
   int nplaced[GC];
   double fp[GC];
@@ -142,6 +144,9 @@ __device__ bool hot_load(Ctx& c, H* h) {
   for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.t->f_loff[f];
   for (int g = c.lane; g < c.G; g += 32) {
     h->sr[g] = c.t->n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0; h->occn[g] = -1;
+    int tot = 0;                     // the node's requesting SM is at most this
+    for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) tot += (int)c.t->p_sm[c.t->s_rl[j]];
+    h->maycut[g] = tot > (int)SM_LIMIT ? 1 : 0;
     h->nplaced[g] = c.t->n_nplaced[g]; h->fp[g] = c.t->n_fp[g];
   }
   for (int g = c.lane; g <= c.G; g += 32) h->seg[g] = c.t->n_seg[g];
@@ -494,7 +499,8 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
     h->key[i] = req ? -(h->qreq[i] - qused) : NOT_REQ;
-    if (req && integral) atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
+    if (req && integral && h->maycut[h->fnode[i] >> 16])
+      atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
     any_req |= req;
   }
   // No pod requests a token: dispatch grants nothing, so coverage, occupancy,
@@ -516,7 +522,8 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     int r = 0;
     // the SM sum ahead is only needed when the node's requesting SM can
     // exceed 100 (otherwise no requesting pod misfits)
-    const bool need_ahead = integral && k != NOT_REQ && h->reqsm[g] > (int)SM_LIMIT;
+    const bool need_ahead = integral && k != NOT_REQ && h->maycut[g] &&
+                            h->reqsm[g] > (int)SM_LIMIT;
     if (need_ahead) {
       double ahead = 0.0;
 #pragma unroll 1
@@ -557,9 +564,13 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
         const double rem = h->qlim[i] - h->qused[i];
         const double dur = rem < quantum ? rem : quantum;
         h->flags[i] |= PF_GRANT;
-        atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
         atomicAdd(&h->ngr[g], 1);
-        if (rem < quantum) atomicOr(&h->ostate[g], 2);
+        if (rem < quantum) {             // partial token: it may set the max duration
+          atomicOr(&h->ostate[g], 2);
+          atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
+        } else {
+          h->covbits[g] = FULL_Q;        // a full quantum is the max (benign race)
+        }
         grants++;
       }
     }
@@ -586,7 +597,8 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
         h->occv[g] = v;
         h->occn[g] = (st & 2) ? -1 : ng;
       }
-      h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
+      const unsigned long long cb = h->covbits[g];
+      h->cov[g] += cb == FULL_Q ? quantum : __longlong_as_double((long long)cb);
       h->occ[g] += v;
     }
   } else {

@@ -35,8 +35,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = ("C2: 4-node cluster, 10 functions (ResNet-50/RNN-T/BERT-shaped), Poisson "
-            "arrivals, heuristic auto-scaling, model sharing, 300 x 1 s windows, policy fast")
+def workload(windows: int) -> str:
+    return ("C2: 4-node cluster, 10 functions (ResNet-50/RNN-T/BERT-shaped), Poisson "
+            f"arrivals, heuristic auto-scaling, model sharing, {windows} x 1 s windows, policy fast")
 METRIC = "simulated scenario-seconds/sec"
 UNIT = "scenario-s/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -251,7 +252,7 @@ def run_reference_arm(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "runs_per_step": sample, "windows": args.windows},
+        "config": {"workload": workload(args.windows), "runs_per_step": sample, "windows": args.windows},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{sample} C2 runs x {args.windows} windows per step "
                                    f"(oracle/gs_oracle.c, {threads} host threads)"},
@@ -354,7 +355,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "runs_per_gpu": args.runs, "windows": args.windows,
+            "config": {"workload": workload(args.windows), "runs_per_gpu": args.runs, "windows": args.windows,
                        "policy": "fast", "l2": "flushed between launches (256 MiB write)",
                        "failed_runs": bad, "summaries_all_gathered": gathered_runs},
             "fleet_summary": fleet_totals(fleet),

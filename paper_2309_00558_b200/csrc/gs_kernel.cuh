@@ -533,18 +533,39 @@ __device__ __noinline__ int best_match(Ctx& c, int slot, int4* chosen) {
   BestKey best;
   best.idx = -1; best.k0 = 0; best.a = best.b = best.d = 0;
   long long scans = 0;
-  #pragma unroll 1
-  for (int g = 0; g < c.G; g++) {
-    if (!admit(c, g, f)) continue;
-    int nf = c.t->n_nfree[g];
-    scans += nf;
+  if (c.G >= 16) {
+    // large fleets: lanes = nodes, so the per-node memory admission checks
+    // (dependent loads) run in parallel; each lane scans its node's list
     #pragma unroll 1
-    for (int j = c.lane; j < nf; j += 32) {
-      int4 r = c.t->n_rect[g * c.R + j];
-      if (rw <= r.z && rh <= r.w) {
-        BestKey k;
-        k.k0 = r_area(r) - rarea; k.a = g; k.b = r.y; k.d = r.x; k.idx = g * c.R + j;
-        if (bk_less(k, best)) best = k;
+    for (int g = c.lane; g < c.G; g += 32) {
+      if (!admit(c, g, f)) continue;
+      const int nf = c.t->n_nfree[g];
+      scans += nf;
+      #pragma unroll 1
+      for (int j = 0; j < nf; j++) {
+        const int4 r = c.t->n_rect[g * c.R + j];
+        if (rw <= r.z && rh <= r.w) {
+          BestKey k;
+          k.k0 = r_area(r) - rarea; k.a = g; k.b = r.y; k.d = r.x; k.idx = g * c.R + j;
+          if (bk_less(k, best)) best = k;
+        }
+      }
+    }
+    scans = warp_sum_ll(scans);
+  } else {
+    #pragma unroll 1
+    for (int g = 0; g < c.G; g++) {
+      if (!admit(c, g, f)) continue;
+      int nf = c.t->n_nfree[g];
+      scans += nf;
+      #pragma unroll 1
+      for (int j = c.lane; j < nf; j += 32) {
+        int4 r = c.t->n_rect[g * c.R + j];
+        if (rw <= r.z && rh <= r.w) {
+          BestKey k;
+          k.k0 = r_area(r) - rarea; k.a = g; k.b = r.y; k.d = r.x; k.idx = g * c.R + j;
+          if (bk_less(k, best)) best = k;
+        }
       }
     }
   }

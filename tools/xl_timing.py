@@ -1,0 +1,12 @@
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["GS_LIB"] = sys.argv[1]
+from paper_2309_00558_b200 import backend, compiler as cc, workloads as wl
+from paper_2309_00558_b200.scenario import Scenario
+backend.LIB_PATH = sys.argv[1]
+b = cc.Batch([cc.compile_run(Scenario.from_dict(wl.c4(s, windows=100)), "fast") for s in range(16)])
+s = backend.Session(b); ms = s.run()
+t = (C.c_ulonglong * 8)()
+backend.lib().gs_xl_timing(t)
+tot = sum(t[:4])
+print(f"{ms:.1f} ms; warp-0 cycles: epoch {t[0]/tot:.2%} window_begin {t[1]/tot:.2%} steps {t[2]/tot:.2%} window_close {t[3]/tot:.2%}")

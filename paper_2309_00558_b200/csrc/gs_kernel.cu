@@ -362,6 +362,18 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
 // XL class driver: warp 0 runs the control code (as simulate_run<void>), all
 // XL_THREADS threads run the quantum steps (gs_xl.cuh).  Every thread calls
 // this with its own Ctx view of the same run.
+// -DGS_XL_TIMING: warp-0 cycle split of the XL driver (tools/xl_timing.py)
+#ifdef GS_XL_TIMING
+__device__ unsigned long long gs_xl_t[8];
+extern "C" int gs_xl_timing(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, gs_xl_t, sizeof(gs_xl_t));
+}
+#define GS_XL_TIC(v) const long long v = clock64()
+#define GS_XL_ADD(k, d) atomicAdd(&gs_xl_t[k], (unsigned long long)(d))
+#else
+#define GS_XL_TIC(v)
+#define GS_XL_ADD(k, d)
+#endif
 __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run,
                                 XlShared* xs) {
   const bool w0 = threadIdx.x < 32;
@@ -399,11 +411,15 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
     if (rebuild) {
       if (w0) {
         bool stop = failed(c);
+        GS_XL_TIC(t0_);
         if (!stop && epoch) {
           run_epoch(c, w);
           stop = failed(c);
         }
+        GS_XL_TIC(t1_);
         if (!stop) window_begin(c, w);
+        GS_XL_TIC(t2_);
+        if (c.lane == 0) { GS_XL_ADD(0, t1_ - t0_); GS_XL_ADD(1, t2_ - t1_); }
         __syncwarp();
         if (c.lane == 0) xs->stop = stop ? 1 : 0;
       }
@@ -416,10 +432,13 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
     for (int g = threadIdx.x; g < c.G; g += blockDim.x) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
     __syncthreads();
     if (xs->stop) break;
+    GS_XL_TIC(t3_);
     #pragma unroll 1
     for (int s = 0; s < c.T; s++) xl_step(c, w, s, xs);
     xl_complete(c);
+    GS_XL_TIC(t4_);
     if (w0) window_close(c, w, out, acc, su, so, peak, fail_total);
+    if (threadIdx.x == 0) { GS_XL_ADD(2, t4_ - t3_); GS_XL_ADD(3, clock64() - t4_); }
     __syncthreads();
   }
   if (w0) finish_run(c, out, host, run, acc, su, so, peak, fail_total, 0, 0, 4, false);

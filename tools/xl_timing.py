@@ -1,3 +1,5 @@
+"""XL driver time split (warp 0): build with `bash tools/build_variant.sh wt xlt -DGS_XL_TIMING`,
+then `python tools/xl_timing.py variants/xlt.so` on the GPU box."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["GS_LIB"] = sys.argv[1]

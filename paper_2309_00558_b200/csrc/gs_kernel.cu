@@ -317,20 +317,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   #pragma unroll 1
   for (int w = 0; w < c.W && !failed(c); w++) {
     const bool epoch = w > 0 && w % c.sc->epoch_windows == 0;
-    if constexpr (std::is_void<H>::value) {     // XL: working set stays in the HBM arena
-      if (epoch) {
-        run_epoch(c, w);
-        if (failed(c)) break;
-      }
-      window_begin(c, w);
-      #pragma unroll 1
-      for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
-      __syncwarp();
-      #pragma unroll 1
-      for (int s = 0; s < c.T; s++) run_step(c, w, s);
-      complete_tokens(c);
-      window_close(c, w, out, acc, su, so, peak, fail_total);
-    } else {
+    {
       // Registration changes only at epochs and when a placed pod warms up;
       // otherwise the shared-memory working set carries over to the next window.
       const bool rebuild = !hot_valid || epoch || w >= c.sh->next_warm;
@@ -351,9 +338,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
       hot_close(c, h, w, out, acc, su, so, peak, fail_total);
     }
   }
-  if constexpr (!std::is_void<H>::value) {
-    if (hot_valid && !c.sh->err) hot_store(c, h);   // flush the last windows' counters
-  }
+  if (hot_valid && !c.sh->err) hot_store(c, h);   // flush the last windows' counters
   finish_run(c, out, host, run, acc, su, so, peak, fail_total, hot_grants, pod_steps,
              class_id<H>(), !std::is_void<H>::value);
 }

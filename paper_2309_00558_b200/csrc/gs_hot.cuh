@@ -269,6 +269,75 @@ __device__ __forceinline__ void hot_admit(H* h, int f, double t0) {
   h->wdrop[f] += drop;
 }
 
+// _serve (sim_engine.py:525-552) for hot pod i of function f, sequentially
+// (the XL working set serves per function; the per-warp classes use the
+// dry-run / scan / replay form below)
+template <class H>
+__device__ __forceinline__ void hot_serve(H* h, int i, int f, double t_start, double t_end) {
+  const double busy = h->busy[i];
+  double t = busy > t_start ? busy : t_start;
+  if (!(t < t_end - TIME_EPS)) { h->busy[i] = t; return; }
+  int fl = h->flags[i];
+  double rem = h->crem[i], arr = h->carr[i];
+  int comp = 0, viol = 0;
+  #pragma unroll 1
+  while (t < t_end - TIME_EPS) {
+    if (!(fl & PF_CUR)) {
+      long long id;
+      const int retn = h->retn[f];
+      const int nsn = h->nsn[f];
+      if (retn > 0) {               // restarted requests precede never-started ones
+        long long* r = &h->f_ret[(size_t)f * h->RET];
+        id = r[0];
+        #pragma unroll 1
+        for (int k = 1; k < retn; k++) r[k - 1] = r[k];
+        h->retn[f] = retn - 1;
+      } else if (nsn > 0) {
+        const int limit = h->maxq[f];
+        if (limit < 0) {
+          int nw = h->nsw[f], ni = h->nsi[f], nn = h->nswn[f];
+          id = pack_id(nw, ni);
+          arr = h->arrival_n(nw, ni, nn);
+          if (nsn > 1) {
+            h->advance(f, nw, ni, nn);
+            h->nsw[f] = nw; h->nsi[f] = ni; h->nswn[f] = nn;
+          }
+        } else {
+          const int hd = h->rhead[f];
+          id = h->f_ring[h->ringoff[f] + hd];
+          h->rhead[f] = (hd + 1) % limit;
+          arr = h->arrival(f, id_w(id), id_i(id));
+        }
+        h->nsn[f] = nsn - 1;
+      } else {
+        break;
+      }
+      if (retn > 0) arr = h->arrival(f, id_w(id), id_i(id));
+      h->pinned[f]++;
+      fl |= PF_CUR;
+      rem = h->invr[i];
+      h->cur[i] = id;
+    }
+    const double left = t_end - t;
+    const double span = rem < left ? rem : left;
+    rem -= span;
+    t += span;
+    if (rem <= TIME_EPS) {
+      h->qlen[f]--;
+      h->pinned[f]--;
+      fl &= ~PF_CUR;
+      comp++;
+      if ((t - arr) * 1000.0 > h->slo[f]) viol++;
+    }
+  }
+  h->busy[i] = t;
+  h->crem[i] = rem;
+  h->carr[i] = arr;
+  h->flags[i] = (unsigned char)fl;
+  h->wcomp[f] += comp;
+  h->wviol[f] += viol;
+}
+
 // id of the `pos`-th unpinned request of function f at the start of the serve
 // phase: restarted (returned) requests first, then never-started ones in
 // queue order (sim_engine.py:531 takes the first request with server None).

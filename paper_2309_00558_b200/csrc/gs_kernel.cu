@@ -16,6 +16,7 @@
 #include "gs_hot.cuh"
 #include "gs_audit.cuh"
 #include "gs_xl.cuh"
+#include "gs_xlh.cuh"
 
 namespace gs {
 
@@ -360,7 +361,7 @@ extern "C" int gs_xl_timing(unsigned long long* out) {
 #define GS_XL_ADD(k, d)
 #endif
 __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run,
-                                XlShared* xs) {
+                                XlShared* xs, HotX* hx, char* xdyn, size_t xbytes) {
   const bool w0 = threadIdx.x < 32;
   Accum acc = {0, 0, 0, 0, 0};
   PySum su, so;
@@ -384,8 +385,15 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
     if (!failed(c)) place_batch(c);
     if (!failed(c)) refresh_frag(c);
   }
+  if (threadIdx.x == 0) {
+    xlh_carve(hx, xdyn, xbytes, c.F, c.G);
+    int bnd = 0;
+    for (int f = 0; f < c.F; f++) bnd |= c.fs[f].max_queue >= 0;
+    hx->bounded = bnd;
+  }
   __syncthreads();
   bool lists_valid = false;            // s_rl / n_seg / s_fl match the registered set
+  bool hot = false;                    // the shared-memory working set holds the run
   #pragma unroll 1
   for (int w = 0; w < c.W; w++) {
     // registration changes only at epochs and warm-ups; otherwise the sorted
@@ -394,6 +402,10 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
     const bool rebuild = !lists_valid || epoch || w >= c.sh->next_warm;
     __syncthreads();                   // everyone read next_warm before warp 0 moves on
     if (rebuild) {
+      if (hot) {                       // write the working set back before the epoch
+        xlh_store(c, hx);
+        hot = false;
+      }
       if (w0) {
         bool stop = failed(c);
         GS_XL_TIC(t0_);
@@ -409,23 +421,46 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
         if (c.lane == 0) xs->stop = stop ? 1 : 0;
       }
       lists_valid = true;
+      __syncthreads();
+      if (xs->stop) break;
+      hot = xlh_load(c, hx);           // false: the registered set does not fit
+    } else if (hot) {
+      xlh_begin_light(hx, w);
+      if (threadIdx.x == 0) { xs->stop = 0; c.sh->pod_steps += (long long)hx->n * c.T; }
     } else {
       xl_begin_light(c, w);
       if (threadIdx.x == 0) xs->stop = 0;
     }
-    #pragma unroll 1
-    for (int g = threadIdx.x; g < c.G; g += blockDim.x) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
+    if (!hot) {
+      #pragma unroll 1
+      for (int g = threadIdx.x; g < c.G; g += blockDim.x) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
+    }
     __syncthreads();
     if (xs->stop) break;
     GS_XL_TIC(t3_);
-    #pragma unroll 1
-    for (int s = 0; s < c.T; s++) xl_step(c, w, s, xs);
-    xl_complete(c);
+    if (hot) {
+      #pragma unroll 1
+      for (int s = 0; s < c.T; s++) {
+        if (hx->bounded) xlh_step<true>(hx, w, s, xs);
+        else xlh_step<false>(hx, w, s, xs);
+        if (threadIdx.x == 0) c.sh->grants += xs->grants;
+      }
+      xlh_complete(hx);
+    } else {
+      #pragma unroll 1
+      for (int s = 0; s < c.T; s++) xl_step(c, w, s, xs);
+      xl_complete(c);
+    }
     GS_XL_TIC(t4_);
-    if (w0) window_close(c, w, out, acc, su, so, peak, fail_total);
+    if (w0) {
+      if (hot) hot_close(c, hx, w, out, acc, su, so, peak, fail_total);
+      else window_close(c, w, out, acc, su, so, peak, fail_total);
+    }
     if (threadIdx.x == 0) { GS_XL_ADD(2, t4_ - t3_); GS_XL_ADD(3, clock64() - t4_); }
     __syncthreads();
   }
+  __syncthreads();
+  if (hot && !c.sh->err) xlh_store(c, hx);     // flush the last windows' state
   if (w0) finish_run(c, out, host, run, acc, su, so, peak, fail_total, 0, 0, 4, false);
   __syncthreads();
 }
@@ -484,6 +519,8 @@ gs_sim_kernel(KArgs a) {
 __global__ void __launch_bounds__(XL_THREADS, 1) gs_sim_kernel_xl(KArgs a) {
   __shared__ WarpShared sh;
   __shared__ XlShared xs;
+  __shared__ HotX hx;
+  extern __shared__ __align__(16) unsigned char xl_dyn[];
   for (;;) {
     if (threadIdx.x == 0) xs.run = atomicAdd(a.counter, 1);
     __syncthreads();
@@ -511,7 +548,7 @@ __global__ void __launch_bounds__(XL_THREADS, 1) gs_sim_kernel_xl(KArgs a) {
       c.Q = 0;
     }
     __syncthreads();
-    simulate_run_xl(c, a.out, a.host, run, &xs);
+    simulate_run_xl(c, a.out, a.host, run, &xs, &hx, reinterpret_cast<char*>(xl_dyn), XLH_DYN_BYTES);
   }
 }
 
@@ -732,9 +769,15 @@ static int launch_class(const KArgs& a, int sms, cudaStream_t st, char* err, siz
 }
 
 static int launch_xl(const KArgs& a, int sms, cudaStream_t st, char* err, size_t err_len) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(gs_sim_kernel_xl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)XLH_DYN_BYTES));
+    attr_set = true;
+  }
   long long blocks = sms;
   if (a.n_order < blocks) blocks = a.n_order > 0 ? a.n_order : 1;
-  gs_sim_kernel_xl<<<(unsigned)blocks, XL_THREADS, 0, st>>>(a);
+  gs_sim_kernel_xl<<<(unsigned)blocks, XL_THREADS, XLH_DYN_BYTES, st>>>(a);
   CK(cudaGetLastError());
   return GS_OK;
 }

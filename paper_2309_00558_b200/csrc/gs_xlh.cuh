@@ -1,0 +1,387 @@
+// gs_xlh.cuh -- the XL class's quantum steps on a CTA-wide shared-memory
+// working set.
+//
+// Same idea as the per-warp classes (gs_hot.cuh), at CTA scale: while the
+// registered set does not change, a run's registered pods (in (node, pod_id)
+// order), functions and nodes live in the CTA's dynamic shared memory (up to
+// ~200 KB: C4's ~10^3 registered pods, 200 functions and 64 nodes take about
+// 140 KB), and all XL_THREADS threads run the steps there with block barriers
+// between phases.  The layout is carved at run time for the run's (F, G) and
+// the largest pod count that fits; a window whose registered set does not fit
+// falls back to the arena-based steps (gs_xl.cuh).  The per-element helpers
+// (hot_admit, hot_serve, hot_close, arrival arithmetic) are the per-warp
+// classes' own, instantiated on this runtime-sized view.
+#pragma once
+#include "gs_hot.cuh"
+#include "gs_xl.cuh"
+
+namespace gs {
+
+// runtime-sized view of the working set (same member names as Hot<>)
+struct HotX {
+  // pods [PC]
+  double *qused, *qreq, *qlim, *sm, *busy, *crem, *carr, *invr, *key;
+  long long* cur;
+  int* fnode;
+  short *order, *flist, *rank;
+  unsigned char* flags;
+  // functions [FC]
+  double *farr, *slo;
+  int *qlen, *pinned, *fw, *fi, *fcnt, *nsn, *nsw, *nsi, *rhead, *retn, *wcomp, *wviol, *wdrop;
+  int *maxq, *ringoff, *fwn, *nswn, *warr, *hn, *loff, *coff;
+  // nodes [GC]
+  double *sr, *cov, *occ, *fp;
+  int *seg, *cut, *reqsm, *ngr, *nplaced;
+  unsigned long long* covbits;
+  // run constants
+  const int32_t* counts;
+  long long* f_ret;
+  long long* f_ring;
+  double ws, qs, quantum;
+  int n, F, G, T, W, RET, integral, bounded, PC;
+
+  __device__ __forceinline__ int count(int f, int w) const { return counts[coff[f] + w]; }
+  __device__ __forceinline__ double dur(int i) const {
+    const double rem = qlim[i] - qused[i];
+    return rem < quantum ? rem : quantum;
+  }
+  __device__ __forceinline__ double arrival(int f, int w, int i) const {
+    return (double)w * ws + ((double)i * ws) / (double)count(f, w);
+  }
+  __device__ __forceinline__ double arrival_n(int w, int i, int n_) const {
+    return (double)w * ws + ((double)i * ws) / (double)n_;
+  }
+  __device__ __forceinline__ void advance(int f, int& w, int& i, int& n_) const {
+    if (++i < n_) return;
+    i = 0;
+    do { w++; n_ = w < W ? count(f, w) : 1; } while (n_ == 0);
+  }
+};
+
+constexpr size_t XLH_DYN_BYTES = 200 * 1024;   // dynamic shared memory per XL CTA
+constexpr size_t XLH_POD_BYTES = 9 * 8 + 8 + 4 + 3 * 2 + 1;   // per registered pod
+constexpr size_t XLH_FN_BYTES = 2 * 8 + 21 * 4 + 4;           // per function (+ loff)
+constexpr size_t XLH_NODE_BYTES = 4 * 8 + 5 * 4 + 8 + 4;      // per node (+ seg)
+
+// upper bound of the carved size (each of the ~50 arrays may pad by < 16 B)
+__host__ __device__ inline size_t xlh_bytes(int PC, int F, int G) {
+  return (size_t)PC * XLH_POD_BYTES + (size_t)(F + 1) * XLH_FN_BYTES
+       + (size_t)(G + 1) * XLH_NODE_BYTES + 64 * 16;
+}
+
+// carve the view over `base` (thread 0 only); PC = largest pod count that fits
+__device__ void xlh_carve(HotX* h, char* base, size_t bytes, int F, int G) {
+  const size_t fixed = xlh_bytes(0, F, G);
+  int PC = bytes > fixed ? (int)((bytes - fixed) / XLH_POD_BYTES) : 0;
+  PC &= ~7;
+  size_t o = 0;
+  auto take = [&](size_t n, size_t elem) { char* p = base + o; o = gs_align16(o + n * elem); return p; };
+  const size_t P = (size_t)PC, Fn = (size_t)F + 1, Gn = (size_t)G + 1;
+  h->qused = (double*)take(P, 8); h->qreq = (double*)take(P, 8); h->qlim = (double*)take(P, 8);
+  h->sm = (double*)take(P, 8); h->busy = (double*)take(P, 8); h->crem = (double*)take(P, 8);
+  h->carr = (double*)take(P, 8); h->invr = (double*)take(P, 8); h->key = (double*)take(P, 8);
+  h->cur = (long long*)take(P, 8); h->fnode = (int*)take(P, 4);
+  h->order = (short*)take(P, 2); h->flist = (short*)take(P, 2); h->rank = (short*)take(P, 2);
+  h->flags = (unsigned char*)take(P, 1);
+  h->farr = (double*)take(Fn, 8); h->slo = (double*)take(Fn, 8);
+  int** fi[] = {&h->qlen, &h->pinned, &h->fw, &h->fi, &h->fcnt, &h->nsn, &h->nsw, &h->nsi,
+                &h->rhead, &h->retn, &h->wcomp, &h->wviol, &h->wdrop, &h->maxq, &h->ringoff,
+                &h->fwn, &h->nswn, &h->warr, &h->hn, &h->loff, &h->coff};
+  for (int k = 0; k < 21; k++) *fi[k] = (int*)take(Fn, 4);
+  h->sr = (double*)take(Gn, 8); h->cov = (double*)take(Gn, 8); h->occ = (double*)take(Gn, 8);
+  h->fp = (double*)take(Gn, 8); h->covbits = (unsigned long long*)take(Gn, 8);
+  h->seg = (int*)take(Gn, 4); h->cut = (int*)take(Gn, 4); h->reqsm = (int*)take(Gn, 4);
+  h->ngr = (int*)take(Gn, 4); h->nplaced = (int*)take(Gn, 4);
+  h->PC = o <= bytes ? PC : 0;
+}
+
+// arena -> working set (all threads); false if the registered set does not fit
+__device__ bool xlh_load(Ctx& c, HotX* h) {
+  const int n = c.sh->n_reg;
+  if (n > h->PC) return false;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int* rl = c.t->s_rl;
+#pragma unroll 1
+  for (int i = tid; i < n; i += NT) {
+    const int s = rl[i];
+    h->qused[i] = c.t->p_qused[s]; h->qreq[i] = c.t->p_qreq[s]; h->qlim[i] = c.t->p_qlim[s];
+    h->sm[i] = c.t->p_sm[s]; h->busy[i] = c.t->p_busy[s]; h->crem[i] = c.t->p_crem[s];
+    h->carr[i] = c.t->p_carr[s]; h->invr[i] = c.t->p_invr[s];
+    h->cur[i] = pack_id(c.t->p_cw[s], c.t->p_ci[s]);
+    h->fnode[i] = c.t->p_fn[s] | (c.t->p_node[s] << 16);
+    h->flags[i] = (unsigned char)(c.t->p_flags[s] & PF_CUR);
+    h->order[i] = (short)i;
+    c.t->s_list[s] = i;                 // slot -> registered index (for flist)
+  }
+#pragma unroll 1
+  for (int f = tid; f < c.F; f += NT) {
+    h->qlen[f] = c.t->f_qlen[f]; h->pinned[f] = c.t->f_pinned[f];
+    h->fw[f] = c.t->f_fw[f]; h->fi[f] = c.t->f_fi[f]; h->fcnt[f] = c.t->f_fn[f];
+    h->nsn[f] = c.t->f_nsn[f]; h->nsw[f] = c.t->f_nsw[f]; h->nsi[f] = c.t->f_nsi[f];
+    h->rhead[f] = c.t->f_rhead[f]; h->retn[f] = c.t->f_retn[f];
+    h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
+    h->warr[f] = c.t->f_warr[f]; h->hn[f] = c.t->f_hn[f];
+    h->maxq[f] = c.fs[f].max_queue;
+    h->ringoff[f] = c.t->f_ringoff[f];
+    h->slo[f] = c.fs[f].slo_ms;
+    h->coff[f] = c.fs[f].count_off;
+    h->farr[f] = h->fcnt[f] > 0 ? arrival_time(c, f, h->fw[f], h->fi[f]) : 0.0;
+    h->fwn[f] = h->fcnt[f] > 0 ? c.count(f, h->fw[f]) : 1;
+    h->nswn[f] = (h->nsn[f] > 0 && c.fs[f].max_queue < 0) ? c.count(f, h->nsw[f]) : 1;
+  }
+#pragma unroll 1
+  for (int f = tid; f <= c.F; f += NT) h->loff[f] = c.t->f_loff[f];
+#pragma unroll 1
+  for (int g = tid; g < c.G; g += NT) {
+    h->sr[g] = c.t->n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0;
+    h->nplaced[g] = c.t->n_nplaced[g]; h->fp[g] = c.t->n_fp[g];
+  }
+#pragma unroll 1
+  for (int g = tid; g <= c.G; g += NT) h->seg[g] = c.t->n_seg[g];
+  if (tid == 0) {
+    h->n = n;
+    h->counts = c.counts; h->f_ret = c.t->f_ret; h->f_ring = c.t->f_ring;
+    h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
+    h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
+    h->integral = c.integral() ? 1 : 0;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int j = tid; j < n; j += NT) h->flist[j] = (short)c.t->s_list[c.t->s_fl[j]];
+  __syncthreads();
+  return true;
+}
+
+// working set -> arena (all threads)
+__device__ void xlh_store(Ctx& c, HotX* h) {
+  const int n = h->n, tid = threadIdx.x, NT = blockDim.x;
+#pragma unroll 1
+  for (int i = tid; i < n; i += NT) {
+    const int s = c.t->s_rl[i];
+    c.t->p_qused[s] = h->qused[i]; c.t->p_busy[s] = h->busy[i];
+    c.t->p_crem[s] = h->crem[i]; c.t->p_carr[s] = h->carr[i];
+    c.t->p_cw[s] = id_w(h->cur[i]); c.t->p_ci[s] = id_i(h->cur[i]);
+    c.t->p_flags[s] = (c.t->p_flags[s] & ~(PF_CUR | PF_GRANT)) | (h->flags[i] & PF_CUR);
+  }
+#pragma unroll 1
+  for (int f = tid; f < c.F; f += NT) {
+    c.t->f_qlen[f] = h->qlen[f]; c.t->f_pinned[f] = h->pinned[f];
+    c.t->f_fw[f] = h->fw[f]; c.t->f_fi[f] = h->fi[f]; c.t->f_fn[f] = h->fcnt[f];
+    c.t->f_nsn[f] = h->nsn[f]; c.t->f_nsw[f] = h->nsw[f]; c.t->f_nsi[f] = h->nsi[f];
+    c.t->f_rhead[f] = h->rhead[f]; c.t->f_retn[f] = h->retn[f];
+    c.t->f_hn[f] = h->hn[f];
+  }
+#pragma unroll 1
+  for (int g = tid; g < c.G; g += NT) c.t->n_sr[g] = h->sr[g];
+  __syncthreads();
+}
+
+// window start without a registration change (cf. hot_begin_light), all threads
+__device__ void xlh_begin_light(HotX* h, int w) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+#pragma unroll 1
+  for (int i = tid; i < h->n; i += NT) h->qused[i] = 0.0;
+#pragma unroll 1
+  for (int f = tid; f < h->F; f += NT) {
+    const int k = h->count(f, w);
+    h->warr[f] = k;
+    if (k > 0) {
+      if (h->fcnt[f] == 0) {
+        h->fw[f] = w; h->fi[f] = 0; h->fwn[f] = k;
+        h->farr[f] = h->arrival_n(w, 0, k);
+      }
+      h->fcnt[f] += k;
+    }
+  }
+#pragma unroll 1
+  for (int g = tid; g < h->G; g += NT) { h->cov[g] = 0.0; h->occ[g] = 0.0; }
+  __syncthreads();
+}
+
+// complete live tokens (sim_engine.py:482-486), all threads
+__device__ void xlh_complete(HotX* h) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (!h->integral) {
+#pragma unroll 1
+    for (int g = tid; g < h->G; g += NT) {
+      double sr = h->sr[g];
+#pragma unroll 1
+      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+        const int i = h->order[j];
+        if (!(h->flags[i] & PF_GRANT)) break;
+        sr -= h->sm[i];
+        if (sr < 0 && sr > -SM_EPS) sr = 0.0;
+      }
+      h->sr[g] = sr;
+    }
+    __syncthreads();
+  }
+#pragma unroll 1
+  for (int i = tid; i < h->n; i += NT) {
+    const int fl = h->flags[i];
+    if (fl & PF_GRANT) {
+      h->qused[i] += h->dur(i);
+      h->flags[i] = (unsigned char)(fl & ~PF_GRANT);
+    }
+  }
+  __syncthreads();
+}
+
+// one quantum step (sim_engine.py:493-520) on the CTA-wide working set
+template <bool BND>
+__device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
+  const double t0 = (double)w * h->ws + (double)s * h->qs;
+  const int n = h->n, F = h->F, G = h->G;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const bool integral = h->integral != 0;
+  if (s > 0 && !integral) {
+    // sm_running -= sm in the last dispatch order, with the float-dust clamp
+#pragma unroll 1
+    for (int g = tid; g < G; g += NT) {
+      double sr = h->sr[g];
+#pragma unroll 1
+      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+        const int i = h->order[j];
+        if (!(h->flags[i] & PF_GRANT)) break;
+        sr -= h->sm[i];
+        if (sr < 0 && sr > -SM_EPS) sr = 0.0;
+      }
+      h->sr[g] = sr;
+    }
+  }
+  if (tid == 0) xs->grants = 0;
+#pragma unroll 1
+  for (int f = tid; f < F; f += NT) hot_admit<HotX, BND>(h, f, t0);
+#pragma unroll 1
+  for (int g = tid; g < G; g += NT) {
+    h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull; h->reqsm[g] = 0; h->ngr[g] = 0;
+  }
+  __syncthreads();
+  // complete live tokens + filter_pods + requesting -> key
+#pragma unroll 1
+  for (int i = tid; i < n; i += NT) {
+    const int f = h->fnode[i] & 0xffff;
+    int fl = h->flags[i];
+    double qused = h->qused[i];
+    if (fl & PF_GRANT) {
+      qused += h->dur(i);
+      h->qused[i] = qused;
+      fl &= ~PF_GRANT;
+      h->flags[i] = (unsigned char)fl;
+    }
+    const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
+    const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
+    h->key[i] = req ? -(h->qreq[i] - qused) : NOT_REQ;
+    if (req && integral) atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
+  }
+  __syncthreads();
+  // build_queue order per node by counting (key, pod index)
+#pragma unroll 1
+  for (int i = tid; i < n; i += NT) {
+    const int g = h->fnode[i] >> 16;
+    const double k = h->key[i];
+    const int lo = h->seg[g], hi = h->seg[g + 1];
+    int r = 0;
+    if (integral && k != NOT_REQ && h->reqsm[g] > (int)SM_LIMIT) {
+      double ahead = 0.0;
+#pragma unroll 1
+      for (int j = lo; j < hi; j++) {
+        const double kj = h->key[j];
+        const bool less = (kj < k) || (kj == k && j < i);
+        r += less;
+        if (less) ahead += h->sm[j];
+      }
+      if (h->sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], r);
+    } else {
+      int j = lo;
+#pragma unroll 1
+      for (; j + 1 < hi; j += 2) {
+        const double a = h->key[j], b = h->key[j + 1];
+        r += (int)(j < i ? a <= k : a < k) + (int)(j + 1 < i ? b <= k : b < k);
+      }
+      if (j < hi) {
+        const double a = h->key[j];
+        r += (int)(j < i ? a <= k : a < k);
+      }
+    }
+    h->order[lo + r] = (short)i;
+    h->rank[i] = (short)r;
+  }
+  __syncthreads();
+  const double quantum = h->quantum;
+  int grants = 0;
+  if (integral) {
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) {
+      const int g = h->fnode[i] >> 16;
+      if (h->key[i] != NOT_REQ && h->rank[i] < h->cut[g]) {
+        const double rem = h->qlim[i] - h->qused[i];
+        const double dur = rem < quantum ? rem : quantum;
+        h->flags[i] |= PF_GRANT;
+        atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
+        atomicAdd(&h->ngr[g], 1);
+        grants++;
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int g = tid; g < G; g += NT) {
+      const int ng = h->ngr[g];
+      if (ng == 0) continue;
+      PySum occ;
+      occ.reset();
+      const int lo = h->seg[g];
+#pragma unroll 1
+      for (int j = lo; j < lo + ng; j++) {
+        const int i = h->order[j];
+        occ.add(h->sm[i] * h->dur(i));
+      }
+      h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
+      h->occ[g] += occ.value() / 100.0;
+    }
+  } else {
+#pragma unroll 1
+    for (int g = tid; g < G; g += NT) {
+      double sr = h->sr[g];
+      double mx = 0.0;
+      PySum occ;
+      occ.reset();
+      int ng = 0;
+#pragma unroll 1
+      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+        const int i = h->order[j];
+        if (h->key[i] == NOT_REQ) break;
+        const double sm = h->sm[i];
+        if (sm + sr > SM_LIMIT + SM_EPS) break;
+        const double rem = h->qlim[i] - h->qused[i];
+        const double dur = rem < quantum ? rem : quantum;
+        h->flags[i] |= PF_GRANT;
+        sr += sm;
+        if (ng == 0 || dur > mx) mx = dur;
+        occ.add(sm * dur);
+        ng++;
+      }
+      h->sr[g] = sr;
+      if (ng) {
+        h->cov[g] += mx;
+        h->occ[g] += occ.value() / 100.0;
+      }
+      grants += ng;
+    }
+  }
+  if (grants) atomicAdd(&xs->grants, grants);
+  __syncthreads();
+  // serve: per function, its granted pods in (node, pod_id) order
+#pragma unroll 1
+  for (int f = tid; f < F; f += NT) {
+    const int e = h->loff[f + 1];
+#pragma unroll 1
+    for (int j = h->loff[f]; j < e; j++) {
+      const int i = h->flist[j];
+      if (h->flags[i] & PF_GRANT) hot_serve(h, i, f, t0, t0 + h->dur(i) * h->ws);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace gs

@@ -206,15 +206,23 @@ def _t_eff(profile) -> float:
 
 
 def _default_caps(scenario, fns) -> Caps:
+    """Static device capacities, sized from the trace peaks so that overflow
+    (a device rerun with larger capacities) stays rare: pods for the whole
+    fleet, and returned requests per function -- a scale-down can hand back
+    one in-flight request per removed pod of the function."""
     window_s = scenario.window_ms / 1000.0
     pods = 8
+    per_fn = 0
     for fn in fns:
         t_eff = _t_eff(fn.profile)
         counts = fn.trace.counts[:scenario.windows]
         peak = max(counts, default=0) / window_s
-        pods += len(fn.initial_pods) + int(math.ceil(1.5 * peak / t_eff)) + 4
+        k = len(fn.initial_pods) + int(math.ceil(1.5 * peak / t_eff)) + 4
+        pods += k
+        per_fn = max(per_fn, k)
     pods = min(max(32, -(-pods // 32) * 32), 1 << 20)
-    return Caps(pods=pods, rects=64, returned=32)
+    returned = min(max(32, -(-per_fn // 32) * 32), 4096)
+    return Caps(pods=pods, rects=64, returned=returned)
 
 
 @dataclass(frozen=True)

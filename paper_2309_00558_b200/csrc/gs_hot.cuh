@@ -107,11 +107,7 @@ __host__ __device__ constexpr bool fits(int n_reg, int F, int G) {
 template <class H>
 __device__ bool hot_load(Ctx& c, H* h) {
   const int n = c.sh->n_reg;
-  if (n > H::PC || c.F > H::FC || c.G > H::GC) {
-    if (c.lane == 0) set_error(c, GS_ERR_CAPACITY, GS_CAP_HOT, n, 0);
-    __syncwarp();
-    return false;
-  }
+  if (n > H::PC || c.F > H::FC || c.G > H::GC) return false;   // window runs on the arena
   for (int i = c.lane; i < n; i += 32) {
     int s = c.t->s_rl[i];
     h->qused[i] = c.t->p_qused[s];

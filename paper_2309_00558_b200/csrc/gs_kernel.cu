@@ -329,14 +329,25 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
           if (failed(c)) break;
         }
         window_begin(c, w);
-        if (!hot_load(c, h)) break;
-        hot_valid = true;
+        hot_valid = hot_load(c, h);
       } else {
         hot_begin_light(h, c.lane, w);
       }
-      pod_steps += (long long)h->n * c.T;
-      hot_grants += hot_steps(h, c.lane, w);
-      hot_close(c, h, w, out, acc, su, so, peak, fail_total);
+      if (hot_valid) {
+        pod_steps += (long long)h->n * c.T;
+        hot_grants += hot_steps(h, c.lane, w);
+        hot_close(c, h, w, out, acc, su, so, peak, fail_total);
+      } else {
+        // the registered set outgrew the class: this window steps on the arena
+        pod_steps += (long long)c.sh->n_reg * c.T;
+        #pragma unroll 1
+        for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
+        __syncwarp();
+        #pragma unroll 1
+        for (int s = 0; s < c.T; s++) run_step(c, w, s);
+        complete_tokens(c);
+        window_close(c, w, out, acc, su, so, peak, fail_total);
+      }
     }
   }
   if (hot_valid && !c.sh->err) hot_store(c, h);   // flush the last windows' counters

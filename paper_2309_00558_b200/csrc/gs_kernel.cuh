@@ -1234,5 +1234,107 @@ __device__ void serve(Ctx& c, int slot, double t_start, double t_end) {
   c.t->f_wviol[f] += viol;
 }
 
+// ----------------------------------------------------------------------------
+// warp-level quantum step on the arena: the fallback for a window whose
+// registered set outgrows the run's shared-memory class (sim_engine.py:493-520)
+// ----------------------------------------------------------------------------
+__device__ void complete_tokens(Ctx& c) {  // _complete_live_tokens (sim_engine.py:482-486)
+  int n = c.sh->n_reg;
+  if (!c.integral()) {
+    // sm_running -= sm in token order per node, with the float-dust clamp
+    #pragma unroll 1
+    for (int g = c.lane; g < c.G; g += 32) {
+      double sr = c.t->n_sr[g];
+      #pragma unroll 1
+      for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) {
+        int slot = c.t->s_rl[c.t->s_ki[j]];
+        if (!(c.t->p_flags[slot] & PF_GRANT)) break;
+        sr -= c.t->p_sm[slot];
+        if (sr < 0 && sr > -SM_EPS) sr = 0.0;
+      }
+      c.t->n_sr[g] = sr;
+    }
+    __syncwarp();
+  }
+  #pragma unroll 1
+  for (int i = c.lane; i < n; i += 32) {
+    int slot = c.t->s_rl[i];
+    int fl = c.t->p_flags[slot];
+    if (fl & PF_GRANT) {
+      c.t->p_qused[slot] += c.t->p_dur[slot];
+      c.t->p_flags[slot] = fl & ~PF_GRANT;
+    }
+  }
+  __syncwarp();
+}
+
+__device__ void run_step(Ctx& c, int w, int s) {
+  const double t0 = (double)w * c.ws + (double)s * c.qs;
+  if (s > 0) complete_tokens(c);   // step 0: window_begin already reset the ledger
+  #pragma unroll 1
+  for (int f = c.lane; f < c.F; f += 32) admit_arrivals(c, f, t0);
+  __syncwarp();
+  // filter_pods + requesting + build_queue keys
+  const int n = c.sh->n_reg;
+  #pragma unroll 1
+  for (int i = c.lane; i < n; i += 32) {
+    int slot = c.t->s_rl[i];
+    int fl = c.t->p_flags[slot];
+    double qused = c.t->p_qused[slot];
+    bool cand = !(c.t->p_qlim[slot] - qused <= QUOTA_EPS);
+    int f = c.t->p_fn[slot];
+    bool req = cand && ((fl & PF_CUR) || (c.t->f_qlen[f] - c.t->f_pinned[f] > 0));
+    c.t->s_ka[i] = ((unsigned long long)c.t->p_node[slot] << 1) | (req ? 0ull : 1ull);
+    c.t->s_kd[i] = req ? ord_key(-(c.t->p_qreq[slot] - qused)) : 0ull;
+    c.t->s_ki[i] = i;
+  }
+  __syncwarp();
+  warp_sort(c, n);
+  // dispatch (head-blocking) + coverage/occupancy, one lane per node
+  int grants = 0;
+  #pragma unroll 1
+  for (int g = c.lane; g < c.G; g += 32) {
+    double sr = c.integral() ? 0.0 : c.t->n_sr[g];
+    double mx = 0.0;
+    PySum occ;
+    occ.reset();
+    int ng = 0;
+    #pragma unroll 1
+    for (int j = c.t->n_seg[g]; j < c.t->n_seg[g + 1]; j++) {
+      if (c.t->s_ka[j] & 1ull) break;           // rest of the node is not requesting
+      int slot = c.t->s_rl[c.t->s_ki[j]];
+      double sm = c.t->p_sm[slot];
+      if (sm + sr > SM_LIMIT + SM_EPS) break;
+      double rem = c.t->p_qlim[slot] - c.t->p_qused[slot];
+      double dur = rem < c.quantum ? rem : c.quantum;
+      c.t->p_dur[slot] = dur;
+      c.t->p_flags[slot] |= PF_GRANT;
+      sr += sm;
+      if (ng == 0 || dur > mx) mx = dur;
+      occ.add(sm * dur);
+      ng++;
+    }
+    if (!c.integral()) c.t->n_sr[g] = sr;
+    if (ng) {
+      c.t->n_cov[g] += mx;
+      c.t->n_occ[g] += occ.value() / 100.0;
+    }
+    grants += ng;
+  }
+  grants = warp_sum_i(grants);
+  if (c.lane == 0) c.sh->grants += grants;
+  __syncwarp();
+  // serve, per function in (node, pod_id) order
+  #pragma unroll 1
+  for (int f = c.lane; f < c.F; f += 32) {
+    #pragma unroll 1
+    for (int j = c.t->f_loff[f]; j < c.t->f_loff[f + 1]; j++) {
+      int slot = c.t->s_fl[j];
+      if (c.t->p_flags[slot] & PF_GRANT) serve(c, slot, t0, t0 + c.t->p_dur[slot] * c.ws);
+    }
+  }
+  __syncwarp();
+}
+
 
 }  // namespace gs

@@ -50,8 +50,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("cuda", "reference"), default="cuda")
-    ap.add_argument("--runs", type=int, default=10656,
-                    help="scenario runs per GPU (3 waves of 24 resident runs x 148 SMs)")
+    ap.add_argument("--runs", type=int, default=21312,
+                    help="scenario runs per GPU (6 waves of 24 resident runs x 148 SMs)")
     ap.add_argument("--windows", type=int, default=300)
     ap.add_argument("--cpu-sample", type=int, default=0,
                     help="runs in the CPU baseline sample (0 = auto)")

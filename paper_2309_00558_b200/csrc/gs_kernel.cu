@@ -230,6 +230,19 @@ __device__ void copy_out_run(const gs_scenario_t& sc, const gs_out_t& out, const
                sizeof(gs_placement_t) * (size_t)nplaced, lane);
 }
 
+// one window stepped on the HBM arena (warp-level; out of line -- it only runs
+// when a run's registered set outgrows its shared-memory class)
+__device__ __noinline__ void arena_window(Ctx& c, int w, const gs_out_t& out, Accum& acc,
+                                          PySum& su, PySum& so, int& peak, int& fail_total) {
+  #pragma unroll 1
+  for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
+  __syncwarp();
+  #pragma unroll 1
+  for (int s = 0; s < c.T; s++) run_step(c, w, s);
+  complete_tokens(c);
+  window_close(c, w, out, acc, su, so, peak, fail_total);
+}
+
 // status, summary, final placements and the zero-copy row copy-out of a
 // finished run (warp-level; lane 0 writes the records)
 __device__ void finish_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run,
@@ -340,13 +353,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
       } else {
         // the registered set outgrew the class: this window steps on the arena
         pod_steps += (long long)c.sh->n_reg * c.T;
-        #pragma unroll 1
-        for (int g = c.lane; g < c.G; g += 32) { c.t->n_cov[g] = 0.0; c.t->n_occ[g] = 0.0; }
-        __syncwarp();
-        #pragma unroll 1
-        for (int s = 0; s < c.T; s++) run_step(c, w, s);
-        complete_tokens(c);
-        window_close(c, w, out, acc, su, so, peak, fail_total);
+        arena_window(c, w, out, acc, su, so, peak, fail_total);
       }
     }
   }

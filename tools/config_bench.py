@@ -33,7 +33,7 @@ def configs(quick: bool):
     c3 = [Scenario.from_dict(wl.c3(s)) for s in range(1024 // k)]
     yield ("C3", "FaST-GShare vs time-sharing sweep: 1024 bursty traces x both policies",
            [x for x in c3 for _ in (0, 1)], ["fast", "timeshare"] * len(c3))
-    n4 = 64 // k
+    n4 = 148 // k            # one XL CTA per SM
     yield ("C4", "64 nodes, 200 functions, diurnal trace, 300 windows",
            [Scenario.from_dict(wl.c4(s, windows=300)) for s in range(n4)], ["fast"] * n4)
     n5 = 12500 // k

@@ -432,15 +432,19 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
           stop = failed(c);
         }
         GS_XL_TIC(t1_);
-        if (!stop) window_begin(c, w);
-        GS_XL_TIC(t2_);
-        if (c.lane == 0) { GS_XL_ADD(0, t1_ - t0_); GS_XL_ADD(1, t2_ - t1_); }
+        if (c.lane == 0) { GS_XL_ADD(0, t1_ - t0_); }
         __syncwarp();
         if (c.lane == 0) xs->stop = stop ? 1 : 0;
       }
       lists_valid = true;
       __syncthreads();
       if (xs->stop) break;
+      GS_XL_TIC(t2_);
+      if (!xl_window_begin(c, w, xdyn, xbytes, xs->warp_tot)) {
+        if (w0) window_begin(c, w);
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) { GS_XL_ADD(1, clock64() - t2_); }
       hot = xlh_load(c, hx);           // false: the registered set does not fit
     } else if (hot) {
       xlh_begin_light(hx, w);

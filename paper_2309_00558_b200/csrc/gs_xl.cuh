@@ -29,6 +29,7 @@ struct XlShared {
   int run;
   int stop;
   int grants;
+  int warp_tot[32];
 };
 
 __device__ __forceinline__ double xl_dur(const Ctx& c, int slot) {

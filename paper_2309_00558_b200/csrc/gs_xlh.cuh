@@ -385,3 +385,164 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
 }
 
 }  // namespace gs
+
+namespace gs {
+
+// ---------------------------------------------------------------------------
+// CTA-wide window begin for the XL class (same results as window_begin):
+// warm-up registration + ledger reset, arrivals, the registered list sorted by
+// (node, pod_id), node segments, per-function lists -- with block sorts in the
+// idle shared-memory block instead of one warp's sort in HBM.
+// ---------------------------------------------------------------------------
+
+// exclusive block scan of one int per thread; returns the total in *total
+__device__ int xl_block_exscan(int v, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;      // inclusive warp prefix
+  }
+  __syncthreads();
+  const int before = wid > 0 ? warp_tot[wid - 1] : 0;
+  *total = warp_tot[nw - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+// block bitonic sort of q (power of two) (a, b, v) triples in shared memory
+__device__ void xl_block_sort(unsigned long long* A, unsigned long long* B, int* V, int q) {
+#pragma unroll 1
+  for (int k = 2; k <= q; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll 1
+      for (int t = threadIdx.x; t < (q >> 1); t += blockDim.x) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int l = i | j;
+        const bool up = (i & k) == 0;
+        const unsigned long long ai = A[i], bi = B[i], al = A[l], bl = B[l];
+        const int vi = V[i], vl = V[l];
+        if (trip_less(al, bl, vl, ai, bi, vi) == up) {
+          A[i] = al; B[i] = bl; V[i] = vl;
+          A[l] = ai; B[l] = bi; V[l] = vi;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// all threads; `scr` = shared scratch of `bytes`.  Returns false when the
+// registered set is too large for the scratch (caller then uses window_begin).
+__device__ bool xl_window_begin(Ctx& c, int w, char* scr, size_t bytes, int* warp_tot) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int phi = pod_high(c);
+  int q = 1;
+  while (q < phi) q <<= 1;
+  if ((size_t)q * 20 > bytes) return false;
+  unsigned long long* A = reinterpret_cast<unsigned long long*>(scr);
+  unsigned long long* B = A + q;
+  int* V = reinterpret_cast<int*>(B + q);
+  __shared__ int next_warm_s;
+  if (tid == 0) next_warm_s = 0x7fffffff;
+  __syncthreads();
+  // warm-up + ledger reset (sim_engine.py:454-460, token_backend.py:213-218);
+  // each thread owns a contiguous chunk of slots so the registered list can be
+  // compacted in slot order
+  const int per = (phi + NT - 1) / NT;
+  const int s0 = tid * per, s1 = min(phi, s0 + per);
+  int nreg = 0, nw = 0x7fffffff;
+#pragma unroll 1
+  for (int slot = s0; slot < s1; slot++) {
+    int fl = c.t->p_flags[slot];
+    if ((fl & PF_PLACED) && !(fl & PF_REG)) {
+      if (c.t->p_warm[slot] <= w) fl |= PF_REG;
+      else nw = min(nw, c.t->p_warm[slot]);
+    }
+    if (fl & PF_REG) { c.t->p_qused[slot] = 0.0; fl &= ~PF_GRANT; nreg++; }
+    c.t->p_flags[slot] = fl;
+  }
+  if (nw != 0x7fffffff) atomicMin(&next_warm_s, nw);
+#pragma unroll 1
+  for (int f = tid; f < c.F; f += NT) {            // _generate_arrivals (:462-470)
+    const int n = c.count(f, w);
+    c.t->f_warr[f] = n;
+    if (n > 0) {
+      if (c.t->f_fn[f] == 0) { c.t->f_fw[f] = w; c.t->f_fi[f] = 0; }
+      c.t->f_fn[f] += n;
+    }
+  }
+  int nr = 0;
+  int pos = xl_block_exscan(nreg, warp_tot, &nr);
+  // registered pods keyed (node, pod_id); padding sorts last
+#pragma unroll 1
+  for (int slot = s0; slot < s1; slot++) {
+    if (!(c.t->p_flags[slot] & PF_REG)) continue;
+    A[pos] = (unsigned long long)c.t->p_node[slot];
+    B[pos] = c.t->p_okey[slot];
+    V[pos] = slot;
+    pos++;
+  }
+#pragma unroll 1
+  for (int i = nr + tid; i < q; i += NT) { A[i] = ~0ull; B[i] = ~0ull; V[i] = 0x7fffffff; }
+  __syncthreads();
+  xl_block_sort(A, B, V, q);
+#pragma unroll 1
+  for (int i = tid; i < nr; i += NT) c.t->s_rl[i] = V[i];
+#pragma unroll 1
+  for (int g = tid; g <= c.G; g += NT) {           // lower bound of node g
+    int lo = 0, hi = nr;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)A[mid] < g) lo = mid + 1; else hi = mid;
+    }
+    c.t->n_seg[g] = lo;
+  }
+  __syncthreads();
+  // per-function lists in (node, pod_id) order: sort (function, list index)
+#pragma unroll 1
+  for (int i = tid; i < q; i += NT) {
+    if (i < nr) {
+      const int slot = V[i];
+      A[i] = (unsigned long long)c.t->p_fn[slot];
+      B[i] = (unsigned long long)i;
+    } else {
+      A[i] = ~0ull; B[i] = ~0ull; V[i] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  xl_block_sort(A, B, V, q);
+#pragma unroll 1
+  for (int i = tid; i < nr; i += NT) c.t->s_fl[i] = V[i];
+#pragma unroll 1
+  for (int f = tid; f <= c.F; f += NT) {
+    int lo = 0, hi = nr;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)A[mid] < f) lo = mid + 1; else hi = mid;
+    }
+    c.t->f_loff[f] = lo;
+  }
+  if (tid == 0) {
+    c.sh->next_warm = next_warm_s;
+    c.sh->n_reg = nr;
+    c.sh->pod_steps += (long long)nr * c.T;
+  }
+  __syncthreads();
+  return true;
+}
+
+}  // namespace gs

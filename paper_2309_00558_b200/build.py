@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libgshare_b200.so")
 SOURCES = ["gs_kernel.cu"]
-DEPS = SOURCES + ["gs_kernel.cuh", "gs_state.cuh", "gs_hot.cuh", "gs_audit.cuh"]
+DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC_FLAGS = [

@@ -368,7 +368,6 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
 // this with its own Ctx view of the same run.
 // -DGS_XL_TIMING: warp-0 cycle split of the XL driver (tools/xl_timing.py)
 #ifdef GS_XL_TIMING
-__device__ unsigned long long gs_xl_t[8];
 extern "C" int gs_xl_timing(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, gs_xl_t, sizeof(gs_xl_t));
 }

@@ -937,7 +937,16 @@ __device__ int ideal_point(const Ctx& c, int f, double residual) {
 // ----------------------------------------------------------------------------
 // epoch: _run_epoch (sim_engine.py:409-430), autoscaler.py:81-160
 // ----------------------------------------------------------------------------
+#ifdef GS_XL_TIMING
+__device__ unsigned long long gs_xl_t[8];   // -DGS_XL_TIMING split (tools/xl_timing.py)
+#define GS_EPOCH_TIC(v) const long long v = clock64()
+#define GS_EPOCH_ADD(k, d) atomicAdd(&gs_xl_t[k], (unsigned long long)(d))
+#else
+#define GS_EPOCH_TIC(v)
+#define GS_EPOCH_ADD(k, d)
+#endif
 __device__ void run_epoch(Ctx& c, int w) {
+  GS_EPOCH_TIC(e0_);
   group_alive_by_fn(c);
   #pragma unroll 1
   for (int f = 0; f < c.F; f++) {
@@ -1029,7 +1038,9 @@ __device__ void run_epoch(Ctx& c, int w) {
     }
     if (failed(c)) return;
   }
+  GS_EPOCH_TIC(e1_);
   place_batch(c);
+  GS_EPOCH_TIC(e2_);
   if (failed(c)) return;
   #pragma unroll 1
   for (int g = 0; g < c.G; g++) {
@@ -1037,6 +1048,8 @@ __device__ void run_epoch(Ctx& c, int w) {
     if (failed(c)) return;
   }
   refresh_frag(c);
+  GS_EPOCH_TIC(e3_);
+  if (c.lane == 0) { GS_EPOCH_ADD(4, e1_ - e0_); GS_EPOCH_ADD(5, e2_ - e1_); GS_EPOCH_ADD(6, e3_ - e2_); }
 }
 
 // ----------------------------------------------------------------------------

@@ -17,18 +17,22 @@
 
 namespace gs {
 
+__device__ int xl_block_exscan(int v, int* warp_tot, int* total);   // below
+
 // runtime-sized view of the working set (same member names as Hot<>)
 struct HotX {
   // pods [PC]
   double *qused, *qreq, *qlim, *sm, *busy, *crem, *carr, *invr, *key;
   long long* cur;
   int* fnode;
-  short *order, *flist, *rank;
+  short *order, *flist, *rank, *gl;   // gl: granted pods in (function, node, pod_id) order
+  int* gpick;                          // request starts of gl[k] (dry run), then its base
   unsigned char* flags;
   // functions [FC]
   double *farr, *slo;
   int *qlen, *pinned, *fw, *fi, *fcnt, *nsn, *nsw, *nsi, *rhead, *retn, *wcomp, *wviol, *wdrop;
   int *maxq, *ringoff, *fwn, *nswn, *warr, *hn, *loff, *coff;
+  int *fbase, *fpicks, *fcomp, *fviol;                 // serve scratch
   // nodes [GC]
   double *sr, *cov, *occ, *fp;
   int *seg, *cut, *reqsm, *ngr, *nplaced;
@@ -59,8 +63,8 @@ struct HotX {
 };
 
 constexpr size_t XLH_DYN_BYTES = 200 * 1024;   // dynamic shared memory per XL CTA
-constexpr size_t XLH_POD_BYTES = 9 * 8 + 8 + 4 + 3 * 2 + 1;   // per registered pod
-constexpr size_t XLH_FN_BYTES = 2 * 8 + 21 * 4 + 4;           // per function (+ loff)
+constexpr size_t XLH_POD_BYTES = 9 * 8 + 8 + 4 + 4 * 2 + 4 + 1;   // per registered pod
+constexpr size_t XLH_FN_BYTES = 2 * 8 + 25 * 4 + 4;           // per function (+ loff)
 constexpr size_t XLH_NODE_BYTES = 4 * 8 + 5 * 4 + 8 + 4;      // per node (+ seg)
 
 // upper bound of the carved size (each of the ~50 arrays may pad by < 16 B)
@@ -83,11 +87,13 @@ __device__ void xlh_carve(HotX* h, char* base, size_t bytes, int F, int G) {
   h->cur = (long long*)take(P, 8); h->fnode = (int*)take(P, 4);
   h->order = (short*)take(P, 2); h->flist = (short*)take(P, 2); h->rank = (short*)take(P, 2);
   h->flags = (unsigned char*)take(P, 1);
+  h->gl = (short*)take(P, 2); h->gpick = (int*)take(P, 4);
   h->farr = (double*)take(Fn, 8); h->slo = (double*)take(Fn, 8);
   int** fi[] = {&h->qlen, &h->pinned, &h->fw, &h->fi, &h->fcnt, &h->nsn, &h->nsw, &h->nsi,
                 &h->rhead, &h->retn, &h->wcomp, &h->wviol, &h->wdrop, &h->maxq, &h->ringoff,
-                &h->fwn, &h->nswn, &h->warr, &h->hn, &h->loff, &h->coff};
-  for (int k = 0; k < 21; k++) *fi[k] = (int*)take(Fn, 4);
+                &h->fwn, &h->nswn, &h->warr, &h->hn, &h->loff, &h->coff,
+                &h->fbase, &h->fpicks, &h->fcomp, &h->fviol};
+  for (int k = 0; k < 25; k++) *fi[k] = (int*)take(Fn, 4);
   h->sr = (double*)take(Gn, 8); h->cov = (double*)take(Gn, 8); h->occ = (double*)take(Gn, 8);
   h->fp = (double*)take(Gn, 8); h->covbits = (unsigned long long*)take(Gn, 8);
   h->seg = (int*)take(Gn, 4); h->cut = (int*)take(Gn, 4); h->reqsm = (int*)take(Gn, 4);
@@ -371,15 +377,104 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
   }
   if (grants) atomicAdd(&xs->grants, grants);
   __syncthreads();
-  // serve: per function, its granted pods in (node, pod_id) order
+  // serve (sim_engine.py:514-552), pod-parallel as in the per-warp classes:
+  // granted pods in (function, node, pod_id) order, a dry run counts each
+  // pod's request starts, a block scan turns them into per-function FIFO
+  // positions, and a replay serves exactly the requests the sequential drain
+  // would hand out.  1. compact the granted pods (chunk per thread, flist order)
+  const double ws = h->ws;
+  const int per = (n + NT - 1) / NT;
+  const int j0 = tid * per, j1 = min(n, j0 + per);
+  int mine = 0;
+#pragma unroll 1
+  for (int j = j0; j < j1; j++) mine += (h->flags[h->flist[j]] & PF_GRANT) ? 1 : 0;
+  int ngl = 0;
+  int k = xl_block_exscan(mine, xs->warp_tot, &ngl);
+#pragma unroll 1
+  for (int j = j0; j < j1; j++) {
+    const int i = h->flist[j];
+    if (h->flags[i] & PF_GRANT) h->gl[k++] = (short)i;
+  }
+#pragma unroll 1
+  for (int f = tid; f < F; f += NT) { h->fcomp[f] = 0; h->fviol[f] = 0; h->fpicks[f] = 0; }
+  __syncthreads();
+  // 2. dry runs (chunk per thread so the block scan below runs in gl order)
+  const int pk = (ngl + NT - 1) / NT;
+  const int k0 = tid * pk, k1 = min(ngl, k0 + pk);
+  int picks = 0;
+#pragma unroll 1
+  for (int kk = k0; kk < k1; kk++) {
+    const int i = h->gl[kk];
+    const int p = serve_dry_run(h, i, t0, t0 + h->dur(i) * ws);
+    h->gpick[kk] = p;
+    picks += p;
+  }
+  int total = 0;
+  int run = xl_block_exscan(picks, xs->warp_tot, &total);
+  // 3. global exclusive prefix of picks per granted pod; each function's
+  //    first granted pod records the prefix where the function starts
+#pragma unroll 1
+  for (int kk = k0; kk < k1; kk++) {
+    const int i = h->gl[kk];
+    const int f = h->fnode[i] & 0xffff;
+    const int p = h->gpick[kk];
+    h->gpick[kk] = run;                       // now: prefix before this pod
+    if (kk == 0 || (h->fnode[h->gl[kk - 1]] & 0xffff) != f) h->fbase[f] = run;
+    atomicAdd(&h->fpicks[f], p);
+    run += p;
+  }
+  __syncthreads();
+  // 4. replay with the pod's FIFO position inside its function
+#pragma unroll 1
+  for (int kk = tid; kk < ngl; kk += NT) {
+    const int i = h->gl[kk];
+    const int f = h->fnode[i] & 0xffff;
+    const double t_end = t0 + h->dur(i) * ws;
+    const int base = h->gpick[kk] - h->fbase[f];
+    const int mypicks = (kk + 1 < ngl ? h->gpick[kk + 1] : total) - h->gpick[kk];
+    int avail = h->retn[f] + h->nsn[f] - base;
+    avail = avail < 0 ? 0 : (avail > mypicks ? mypicks : avail);
+    int comp = 0, viol = 0;
+    serve_replay<HotX, BND>(h, i, f, t0, t_end, base, avail, comp, viol);
+    if (comp) atomicAdd(&h->fcomp[f], comp);
+    if (viol) atomicAdd(&h->fviol[f], viol);
+  }
+  __syncthreads();
+  // 5. each function's queue bookkeeping once
 #pragma unroll 1
   for (int f = tid; f < F; f += NT) {
-    const int e = h->loff[f + 1];
-#pragma unroll 1
-    for (int j = h->loff[f]; j < e; j++) {
-      const int i = h->flist[j];
-      if (h->flags[i] & PF_GRANT) hot_serve(h, i, f, t0, t0 + h->dur(i) * h->ws);
+    const int want = h->fpicks[f];
+    const int comp = h->fcomp[f];
+    if (want == 0 && comp == 0) continue;
+    const int avail = h->retn[f] + h->nsn[f];
+    const int taken = want < avail ? want : avail;
+    const int retn = h->retn[f];
+    const int from_ret = taken < retn ? taken : retn;
+    const int from_ns = taken - from_ret;
+    if (from_ret) {
+      long long* r = &h->f_ret[(size_t)f * h->RET];
+      for (int q = from_ret; q < retn; q++) r[q - from_ret] = r[q];
+      h->retn[f] = retn - from_ret;
     }
+    if (from_ns) {
+      const int nsn = h->nsn[f] - from_ns;
+      h->nsn[f] = nsn;
+      const int limit = BND ? h->maxq[f] : -1;
+      if (limit >= 0) {
+        h->rhead[f] = (h->rhead[f] + from_ns) % limit;
+      } else if (nsn > 0) {
+        int w2 = h->nsw[f], i2 = h->nsi[f] + from_ns, n2 = h->nswn[f];
+        while (i2 >= n2) {
+          i2 -= n2;
+          do { w2++; n2 = h->count(f, w2); } while (n2 == 0);
+        }
+        h->nsw[f] = w2; h->nsi[f] = i2; h->nswn[f] = n2;
+      }
+    }
+    h->pinned[f] += taken - comp;
+    h->qlen[f] -= comp;
+    h->wcomp[f] += comp;
+    h->wviol[f] += h->fviol[f];
   }
   __syncthreads();
 }

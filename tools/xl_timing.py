@@ -12,3 +12,5 @@ t = (C.c_ulonglong * 8)()
 backend.lib().gs_xl_timing(t)
 tot = sum(t[:4])
 print(f"{ms:.1f} ms; warp-0 cycles: epoch {t[0]/tot:.2%} window_begin {t[1]/tot:.2%} steps {t[2]/tot:.2%} window_close {t[3]/tot:.2%}")
+ep = max(t[0], 1)
+print(f"  epoch split: scaling {t[4]/ep:.1%}  place_batch {t[5]/ep:.1%}  restructure+frag {t[6]/ep:.1%}")

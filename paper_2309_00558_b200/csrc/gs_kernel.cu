@@ -423,16 +423,16 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
         xlh_store(c, hx);
         hot = false;
       }
-      if (w0) {
-        bool stop = failed(c);
-        GS_XL_TIC(t0_);
-        if (!stop && epoch) {
-          run_epoch(c, w);
-          stop = failed(c);
+      GS_XL_TIC(t0_);
+      if (epoch && !c.sh->err) {       // decisions on every warp, applied by warp 0
+        if (!xl_run_epoch(c, w, xdyn, xbytes, xs)) {
+          if (w0) run_epoch(c, w);
         }
+      }
+      if (w0) {
+        const bool stop = failed(c);
         GS_XL_TIC(t1_);
         if (c.lane == 0) { GS_XL_ADD(0, t1_ - t0_); }
-        __syncwarp();
         if (c.lane == 0) xs->stop = stop ? 1 : 0;
       }
       lists_valid = true;

@@ -685,6 +685,14 @@ __device__ bool place_pod(Ctx& c, int slot, int g, int4 chosen) {
   return true;
 }
 
+#ifdef GS_XL_TIMING
+__device__ unsigned long long gs_xl_t[16];   // -DGS_XL_TIMING split (tools/xl_timing.py)
+#define GS_EPOCH_TIC(v) const long long v = clock64()
+#define GS_EPOCH_ADD(k, d) atomicAdd(&gs_xl_t[k], (unsigned long long)(d))
+#else
+#define GS_EPOCH_TIC(v)
+#define GS_EPOCH_ADD(k, d)
+#endif
 // _place_batch: sim_engine.py:394-407.  Batch = every alive, unplaced pod
 // (the retry list plus this epoch's additions); order (-area, pod_id).
 __device__ void place_batch(Ctx& c) {
@@ -726,8 +734,11 @@ __device__ void place_batch(Ctx& c) {
     const int slot = c.t->s_batch[i];
     int4 chosen;
     const long long before = c.sh->rect_scans;
+    GS_EPOCH_TIC(b0_);
     const int g = best_match(c, slot, &chosen);
     __syncwarp();
+    GS_EPOCH_TIC(b1_);
+    if (c.lane == 0) { GS_EPOCH_ADD(7, b1_ - b0_); }
     if (g >= 0) {
       if (c.lane == 0) c.sh->attempts++;
       if (!place_pod(c, slot, g, chosen)) return;
@@ -937,14 +948,6 @@ __device__ int ideal_point(const Ctx& c, int f, double residual) {
 // ----------------------------------------------------------------------------
 // epoch: _run_epoch (sim_engine.py:409-430), autoscaler.py:81-160
 // ----------------------------------------------------------------------------
-#ifdef GS_XL_TIMING
-__device__ unsigned long long gs_xl_t[8];   // -DGS_XL_TIMING split (tools/xl_timing.py)
-#define GS_EPOCH_TIC(v) const long long v = clock64()
-#define GS_EPOCH_ADD(k, d) atomicAdd(&gs_xl_t[k], (unsigned long long)(d))
-#else
-#define GS_EPOCH_TIC(v)
-#define GS_EPOCH_ADD(k, d)
-#endif
 __device__ void run_epoch(Ctx& c, int w) {
   GS_EPOCH_TIC(e0_);
   group_alive_by_fn(c);

@@ -640,4 +640,624 @@ __device__ bool xl_window_begin(Ctx& c, int w, char* scr, size_t bytes, int* war
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// XL epoch (sim_engine.py:409-430, autoscaler.py:81-160) on the whole CTA.
+//
+// A function's scaling decision reads only its own running set, its request
+// history and its profile, so the decisions are independent: every warp
+// decides functions wid, wid + 16, ... (sort of the running set by
+// (efficiency, pod_id), Python sum of the throughputs, scale-up count + ideal
+// point, or the scale-down prefix length) into a per-function record, and
+// warp 0 then applies the records in function order -- the make_pod /
+// remove_pod sequence, slot reuse, decision counter and first error are
+// exactly the sequential loop's.  place_batch / restructure stay on warp 0.
+// ---------------------------------------------------------------------------
+
+// ascending bitonic sort of n (a, b, v) triples in (warp-private) memory
+__device__ void xl_warp_sort_mem(unsigned long long* A, unsigned long long* B, int* V, int n,
+                                 int lane) {
+  int q = 1;
+  while (q < n) q <<= 1;
+#pragma unroll 1
+  for (int i = n + lane; i < q; i += 32) { A[i] = ~0ull; B[i] = ~0ull; V[i] = 0x7fffffff; }
+  __syncwarp();
+#pragma unroll 1
+  for (int k = 2; k <= q; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll 1
+      for (int t = lane; t < (q >> 1); t += 32) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int l = i | j;
+        const bool up = (i & k) == 0;
+        const unsigned long long ai = A[i], bi = B[i], al = A[l], bl = B[l];
+        const int vi = V[i], vl = V[l];
+        if (trip_less(al, bl, vl, ai, bi, vi) == up) {
+          A[i] = al; B[i] = bl; V[i] = vl;
+          A[l] = ai; B[l] = bi; V[l] = vi;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// decision of function f by one warp; the running set s_list[f_loff[f] ..)
+// is left sorted in place.  kind: 0 none, 1 up (cnt, ideal), 2 down (nrem).
+__device__ void xl_decide(Ctx& c, int f, int* kind, int* ideal_o, int* nrem_o, long long* cnt_o,
+                          unsigned long long* A, unsigned long long* B, int* V) {
+  const int lane = c.lane;
+  const int start = c.t->f_loff[f];
+  const int n = c.t->f_loff[f + 1] - start;
+  int* lst = c.t->s_list + start;
+  double thr = 0.0;
+  PySum sup;
+  sup.reset();
+  if (n <= 32) {
+    unsigned long long a = ~0ull, b = ~0ull;
+    int v = 0x7fffffff;
+    if (lane < n) {
+      const int slot = lst[lane];
+      a = ord_key(c.pt(f, c.t->p_pt[slot]).rpr);
+      b = c.t->p_okey[slot];
+      v = slot;
+    }
+    warp_sort_regs(a, b, v, n, lane);
+    __syncwarp();
+    if (lane < n) {
+      thr = c.pt(f, c.t->p_pt[v]).thr;
+      lst[lane] = v;
+    }
+#pragma unroll 1
+    for (int i = 0; i < n; i++) sup.add(__shfl_sync(FULL, thr, i));
+  } else {
+#pragma unroll 1
+    for (int i = lane; i < n; i += 32) {
+      const int slot = lst[i];
+      A[i] = ord_key(c.pt(f, c.t->p_pt[slot]).rpr);
+      B[i] = c.t->p_okey[slot];
+      V[i] = slot;
+    }
+    __syncwarp();
+    xl_warp_sort_mem(A, B, V, n, lane);
+#pragma unroll 1
+    for (int i = lane; i < n; i += 32) lst[i] = V[i];
+#pragma unroll 1
+    for (int i = 0; i < n; i++) sup.add(c.pt(f, c.t->p_pt[V[i]]).thr);
+  }
+  const int hn = c.t->f_hn[f];
+  const double* h = &c.t->f_hist[3 * f];
+  double pred = h[(hn - 1) % 3];              // max(history[-3:])
+#pragma unroll 1
+  for (int k = 2; k <= 3 && k <= hn; k++) {
+    const double x = h[(hn - k) % 3];
+    if (x > pred) pred = x;
+  }
+  const double gap = pred - sup.value();      // rps_gap
+  int kd = 0, idl = -1, nrem = 0;
+  long long cnt = 0;
+  if (gap > 0) {                              // scale_up: autoscaler.py:103-131
+    const int pe = c.fs[f].p_eff;
+    const double t_eff = c.pt(f, pe).thr;
+    const double nd = floor(gap / t_eff);
+    const double residual = gap - nd * t_eff;
+    cnt = (long long)nd;
+    if (residual > 0) {
+      idl = ideal_point(c, f, residual);
+      if (idl < 0) idl = pe;
+    }
+    kd = 1;
+  } else if (gap < 0) {                       // scale_down: autoscaler.py:134-149
+    double delta = gap;
+#pragma unroll 1
+    for (int i = 0; i < n && delta < 0; i++) {
+      const double t = n <= 32 ? __shfl_sync(FULL, thr, i) : c.pt(f, c.t->p_pt[V[i]]).thr;
+      if (delta + t > 0) break;
+      delta += t;
+      nrem++;
+    }
+    kd = 2;
+  }
+  if (lane == 0) { kind[f] = kd; ideal_o[f] = idl; nrem_o[f] = nrem; cnt_o[f] = cnt; }
+  __syncwarp();
+}
+
+// _carve + _subdivide + _prune_contained (packer.py:196-242) on the whole
+// CTA: the split parts are compacted in (rect, part) order into shared `tmp`,
+// each warp decides containment for its rects (lanes over the others), and
+// the survivors are written back to `list` in order.  Returns the new count,
+// or -1 (list untouched) when it would exceed `cap` -- carve()'s contract.
+__device__ int xl_carve(int4* list, int n, int4 placed, int cap, int4* tmp, int* kpos,
+                        int* warp_tot) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = NT >> 5;
+  int m = 0;
+#pragma unroll 1
+  for (int s0 = 0; s0 < n; s0 += NT) {
+    const int j = s0 + tid;
+    int4 parts[4];
+    int np = 0;
+    if (j < n) {
+      const int4 r = list[j];
+      if (!r_intersects(r, placed)) {
+        parts[np++] = r;
+      } else {
+        const int ix = max(r.x, placed.x), iy = max(r.y, placed.y);
+        const int ix2 = min(r.x + r.z, placed.x + placed.z);
+        const int iy2 = min(r.y + r.w, placed.y + placed.w);
+        if (ix > r.x) parts[np++] = make_int4(r.x, r.y, ix - r.x, r.w);
+        if (ix2 < r.x + r.z) parts[np++] = make_int4(ix2, r.y, r.x + r.z - ix2, r.w);
+        if (iy > r.y) parts[np++] = make_int4(r.x, r.y, r.z, iy - r.y);
+        if (iy2 < r.y + r.w) parts[np++] = make_int4(r.x, iy2, r.z, r.y + r.w - iy2);
+      }
+    }
+    int tot;
+    const int off = m + xl_block_exscan(np, warp_tot, &tot);
+#pragma unroll 1
+    for (int k = 0; k < np; k++) tmp[off + k] = parts[k];
+    m += tot;
+  }
+  __syncthreads();
+  // prune: drop rects contained in another; exact duplicates keep the first
+#pragma unroll 1
+  for (int i = wid; i < m; i += nw) {
+    const int4 r = tmp[i];
+    bool kill = false;
+#pragma unroll 1
+    for (int j0 = 0; j0 < m && !kill; j0 += 32) {
+      const int j = j0 + lane;
+      bool k = false;
+      if (j < m && j != i) {
+        const int4 o = tmp[j];
+        k = r_contains(o, r) && !(r_eq(r, o) && i < j);
+      }
+      kill = __any_sync(FULL, k);
+    }
+    if (lane == 0) kpos[i] = kill ? 0 : 1;
+  }
+  __syncthreads();
+  int kept = 0;
+#pragma unroll 1
+  for (int s0 = 0; s0 < m; s0 += NT) {
+    const int i = s0 + tid;
+    const int kf = i < m ? kpos[i] : 0;
+    int tot;
+    const int off = kept + xl_block_exscan(kf, warp_tot, &tot);
+    if (kf) kpos[i] = (off << 1) | 1;
+    kept += tot;
+  }
+  if (kept > cap) return -1;                   // uniform: kept is the block total
+  __syncthreads();
+#pragma unroll 1
+  for (int i = tid; i < m; i += NT) {
+    const int kp = kpos[i];
+    if (kp & 1) list[kp >> 1] = tmp[i];
+  }
+  return kept;
+}
+
+// footprint (memory_model.py:60-72) of node g on one warp: the terms are
+// formed lane-parallel and added in resident (dict insertion) order, so the
+// double equals refresh_footprint's sequential loop.
+__device__ void xl_footprint(Ctx& c, int g) {
+  const int lane = c.lane;
+  const int2* res = &c.t->n_res[g * c.F];
+  const int nres = c.t->n_nres[g];
+  const bool sharing = (c.flags & GS_FLAG_SHARING) != 0;
+  double total = 0.0;
+#pragma unroll 1
+  for (int i0 = 0; i0 < nres; i0 += 32) {
+    const int i = i0 + lane;
+    double term = 0.0;
+    bool use = false;
+    if (i < nres) {
+      const int2 e = res[i];
+      if (e.y > 0) {
+        const gs_function_t& fs = c.fs[e.x];
+        term = sharing ? fs.mem_server_mb + (double)e.y * fs.mem_runtime_mb
+                       : (double)e.y * fs.mem_noshare_mb;
+        use = true;
+      }
+    }
+    const unsigned m = __ballot_sync(FULL, use);
+    const int lim = min(32, nres - i0);
+#pragma unroll 1
+    for (int k = 0; k < lim; k++) {
+      const double t = __shfl_sync(FULL, term, k);
+      if ((m >> k) & 1u) total += t;
+    }
+  }
+  if (lane == 0) c.t->n_fp[g] = total;
+  __syncwarp();
+}
+
+// memory_model.add_pod (memory_model.py:49-50) + footprint, one warp
+__device__ void xl_mem_add(Ctx& c, int g, int f) {
+  const int lane = c.lane;
+  int* cnt = &c.t->n_cnt[g * c.F + f];
+  int2* res = &c.t->n_res[g * c.F];
+  const int nres = c.t->n_nres[g];
+  const int had = *cnt;
+  if (had > 0) {
+#pragma unroll 1
+    for (int i0 = 0; i0 < nres; i0 += 32) {
+      const int i = i0 + lane;
+      const unsigned m = __ballot_sync(FULL, i < nres && res[i].x == f);
+      if (m) {
+        if (lane == __ffs(m) - 1) res[i].y++;
+        break;
+      }
+    }
+  } else if (lane == 0) {
+    res[nres] = make_int2(f, 1);
+    c.t->n_nres[g] = nres + 1;
+  }
+  if (lane == 0) *cnt = had + 1;
+  __syncwarp();
+  xl_footprint(c, g);
+}
+
+// memory_model.remove_pod (memory_model.py:52-58) + footprint, one warp:
+// `del resident[f]` keeps the order of the others
+__device__ void xl_mem_remove(Ctx& c, int g, int f) {
+  const int lane = c.lane;
+  int* cnt = &c.t->n_cnt[g * c.F + f];
+  int2* res = &c.t->n_res[g * c.F];
+  const int nres = c.t->n_nres[g];
+  int at = -1;
+#pragma unroll 1
+  for (int i0 = 0; i0 < nres; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned m = __ballot_sync(FULL, i < nres && res[i].x == f);
+    if (m) { at = i0 + __ffs(m) - 1; break; }
+  }
+  if (at >= 0) {
+    const int2 e = res[at];
+    if (e.y == 1) {
+#pragma unroll 1
+      for (int j0 = at; j0 + 1 < nres; j0 += 32) {   // shift left, chunk by chunk
+        const int j = j0 + lane;
+        int2 nx = make_int2(0, 0);
+        if (j + 1 < nres) nx = res[j + 1];
+        __syncwarp();
+        if (j + 1 < nres) res[j] = nx;
+        __syncwarp();
+      }
+      if (lane == 0) c.t->n_nres[g] = nres - 1;
+    } else if (lane == 0) {
+      res[at].y = e.y - 1;
+    }
+  }
+  if (lane == 0) (*cnt)--;
+  __syncwarp();
+  xl_footprint(c, g);
+}
+
+// _remove_pod (sim_engine.py:377-392), one warp; same effects and error
+// order as remove_pod
+__device__ void xl_remove_pod(Ctx& c, int slot) {
+  const int fl = c.t->p_flags[slot];
+  if (fl & PF_RETRY) {
+    if (c.lane == 0) free_slot(c, slot);
+    __syncwarp();
+    return;
+  }
+  const int f = c.t->p_fn[slot];
+  const int g = c.t->p_node[slot];
+  int ok = 1;
+  if (c.lane == 0) {
+    if (fl & PF_CUR) {
+      return_request(c, f, pack_id(c.t->p_cw[slot], c.t->p_ci[slot]));
+      c.t->f_pinned[f]--;
+    }
+    const int n = c.t->n_nfree[g];
+    if (n >= c.R) {
+      set_error(c, GS_ERR_CAPACITY, GS_CAP_RECTS, g, 0);
+      ok = 0;
+    } else {
+      c.t->n_rect[g * c.R + n] =
+          make_int4(c.t->p_x[slot], c.t->p_y[slot], c.t->p_w[slot], c.t->p_h[slot]);
+      c.t->n_nfree[g] = n + 1;
+    }
+  }
+  ok = __shfl_sync(FULL, ok, 0);
+  if (!ok) return;
+  xl_mem_remove(c, g, f);
+  if (c.lane == 0) {
+    c.t->n_nplaced[g]--;
+    free_slot(c, slot);
+  }
+  __syncwarp();
+}
+
+// scale_up's pod creations for one function (autoscaler.py:103-131 ->
+// _make_pod, sim_engine.py:337-368), one warp: pod i takes the i-th slot off
+// the free stack and pod counter pctr + i, exactly as `total` sequential
+// make_pod calls; the first failing call (zero-rate point, empty stack) stops
+// the sequence with make_pod's error.
+__device__ void xl_make_pods(Ctx& c, int f, long long n_eff, int ideal, int warm) {
+  const int lane = c.lane;
+  const gs_function_t& fs = c.fs[f];
+  const int pe = fs.p_eff;
+  const long long total = n_eff + (ideal >= 0 ? 1 : 0);
+  const int top = c.sh->free_top;
+  const bool pe_ok = c.pt(f, pe).rate_ok != 0;
+  const bool id_ok = ideal < 0 || c.pt(f, ideal).rate_ok != 0;
+  // first failing index and its error
+  long long stop = total;
+  int code = 0, detail = 0, a0 = 0, a1 = 0;
+  if (n_eff > 0 && !pe_ok) { stop = 0; code = GS_ERR_VALIDATION; a0 = f; a1 = pe; }
+  else if (ideal >= 0 && !id_ok) { stop = n_eff; code = GS_ERR_VALIDATION; a0 = f; a1 = ideal; }
+  if (top < stop) { stop = top; code = GS_ERR_CAPACITY; detail = GS_CAP_PODS; a0 = c.P; a1 = 0; }
+  const int made = (int)stop;
+  const int ctr0 = c.t->f_pctr[f];
+  const unsigned long long okey0 = (unsigned long long)fs.id_rank * POW11_10;
+#pragma unroll 1
+  for (int i = lane; i < made; i += 32) {
+    const int k = i < n_eff ? pe : ideal;
+    const gs_point_t& p = c.pt(f, k);
+    const int slot = c.t->s_free[top - 1 - i];
+    const int ctr = ctr0 + i;
+    c.t->p_fn[slot] = f; c.t->p_pt[slot] = k; c.t->p_node[slot] = -1; c.t->p_flags[slot] = PF_ALIVE;
+    c.t->p_warm[slot] = warm; c.t->p_ctr[slot] = ctr; c.t->p_x[slot] = 0; c.t->p_y[slot] = 0;
+    c.t->p_w[slot] = p.rect_w; c.t->p_h[slot] = p.rect_h; c.t->p_cw[slot] = 0; c.t->p_ci[slot] = 0;
+    c.t->p_okey[slot] = okey0 + digits_key(ctr);
+    c.t->p_sm[slot] = p.sm_eff;
+    c.t->p_qlim[slot] = p.quota;
+    c.t->p_qreq[slot] = p.quota;
+    c.t->p_qused[slot] = 0.0; c.t->p_busy[slot] = 0.0; c.t->p_invr[slot] = p.inv_rate;
+    c.t->p_crem[slot] = 0.0; c.t->p_carr[slot] = 0.0; c.t->p_dur[slot] = 0.0;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    c.sh->free_top = top - made;
+    if (c.sh->free_top < c.sh->min_free) c.sh->min_free = c.sh->free_top;
+    c.t->f_pctr[f] = ctr0 + made;
+    if (code) set_error(c, code, detail, a0, a1);
+  }
+  __syncwarp();
+}
+
+// _place_batch (sim_engine.py:394-407) on the whole CTA: the batch is
+// compacted and sorted (-area, pod_id) in shared memory by every thread, and
+// each request's best_match (packer.py:169-193) scans the fleet's free rects
+// with all threads -- tpn threads per node, a block argmin over the same
+// (area gap, node, y, x, list index) key, so the choice is the warp
+// version's; every warp reduces the per-warp winners itself, so the whole CTA
+// follows the same sequence of decisions.  The carve runs CTA-wide
+// (xl_carve); the memory ledger and the pod's fields are one thread's.
+// Returns false when the batch or a node's split list does not fit the
+// scratch (caller runs place_batch).
+__device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = NT >> 5;
+  const int phi = pod_high(c);
+  int q = 1;
+  while (q < phi) q <<= 1;
+  const size_t carve_n = 4 * (size_t)c.R + 8;
+  if ((size_t)q * 20 + carve_n * 20 > bytes) return false;
+  unsigned long long* A = reinterpret_cast<unsigned long long*>(scr);
+  unsigned long long* B = A + q;
+  int4* tmp = reinterpret_cast<int4*>(B + q);
+  int* V = reinterpret_cast<int*>(tmp + carve_n);
+  int* kpos = V + q;
+  __shared__ BestKey wbest[32];
+  __shared__ long long wscan[32];
+  // batch = alive, unplaced pods, compacted in slot order
+  const int per = (phi + NT - 1) / NT;
+  const int s0 = tid * per, s1 = min(phi, s0 + per);
+  int mine = 0;
+#pragma unroll 1
+  for (int slot = s0; slot < s1; slot++)
+    mine += (c.t->p_flags[slot] & (PF_ALIVE | PF_PLACED)) == PF_ALIVE;
+  int nb = 0;
+  int pos = xl_block_exscan(mine, warp_tot, &nb);
+#pragma unroll 1
+  for (int slot = s0; slot < s1; slot++) {
+    const int fl = c.t->p_flags[slot];
+    if ((fl & (PF_ALIVE | PF_PLACED)) != PF_ALIVE) continue;
+    A[pos] = ~(unsigned long long)((long long)c.t->p_w[slot] * c.t->p_h[slot]);   // descending area
+    B[pos] = c.t->p_okey[slot];
+    V[pos] = slot;
+    c.t->p_flags[slot] = fl & ~PF_RETRY;
+    pos++;
+  }
+  int qb = 1;
+  while (qb < nb) qb <<= 1;
+#pragma unroll 1
+  for (int i = nb + tid; i < qb; i += NT) { A[i] = ~0ull; B[i] = ~0ull; V[i] = 0x7fffffff; }
+  __syncthreads();
+  GS_EPOCH_TIC(p0_);
+  xl_block_sort(A, B, V, qb);
+  // entry i's best_match inputs: A = (w, h), B = function
+#pragma unroll 1
+  for (int i = tid; i < nb; i += NT) {
+    const int slot = V[i];
+    A[i] = ((unsigned long long)(unsigned)c.t->p_w[slot] << 32) | (unsigned)c.t->p_h[slot];
+    B[i] = (unsigned long long)c.t->p_fn[slot];
+  }
+  int tpn = 1;                                 // threads per node (power of two)
+  while (tpn * 2 * c.G <= NT && tpn < 32) tpn <<= 1;
+  const int sub = tid & (tpn - 1);
+  const int gstride = NT / tpn;
+  __syncthreads();
+  GS_EPOCH_TIC(p1_);
+  if (tid == 0) { GS_EPOCH_ADD(8, p1_ - p0_); }
+  int i = 0;
+#pragma unroll 1
+  while (i < nb) {
+    GS_EPOCH_TIC(p2_);
+    const unsigned long long wh = A[i];
+    const int f = (int)B[i];
+    const int rw = (int)(wh >> 32), rh = (int)(wh & 0xffffffffu);
+    const long long rarea = (long long)rw * rh;
+    BestKey best;
+    best.idx = -1; best.k0 = 0; best.a = best.b = best.d = 0;
+    long long scans = 0;
+#pragma unroll 1
+    for (int g = tid / tpn; g < c.G; g += gstride) {
+      if (!admit(c, g, f)) continue;
+      const int nf = c.t->n_nfree[g];
+      if (sub == 0) scans += nf;
+      const int4* rl = &c.t->n_rect[g * c.R];
+#pragma unroll 1
+      for (int j = sub; j < nf; j += tpn) {
+        const int4 r = rl[j];
+        if (rw <= r.z && rh <= r.w) {
+          BestKey k;
+          k.k0 = r_area(r) - rarea; k.a = g; k.b = r.y; k.d = r.x; k.idx = g * c.R + j;
+          if (bk_less(k, best)) best = k;
+        }
+      }
+    }
+    best = warp_argmin(best);
+    scans = warp_sum_ll(scans);
+    if (lane == 0) { wbest[wid] = best; wscan[wid] = scans; }
+    __syncthreads();
+    GS_EPOCH_TIC(p3_);
+    if (tid == 0) { GS_EPOCH_ADD(11, p3_ - p2_); GS_EPOCH_ADD(10, 1); }
+    BestKey k;                                 // every warp: the block winner
+    k.idx = -1; k.k0 = 0; k.a = k.b = k.d = 0;
+    long long sc = 0;
+    if (lane < nw) { k = wbest[lane]; sc = wscan[lane]; }
+    k = warp_argmin(k);
+    sc = warp_sum_ll(sc);
+    if (k.idx >= 0) {
+      const int g = k.a;
+      const int4 chosen = c.t->n_rect[k.idx];
+      const int n = c.t->n_nfree[g];
+      if (tid == 0) { c.sh->rect_scans += sc; c.sh->attempts++; }
+      const int nn = xl_carve(&c.t->n_rect[g * c.R], n, make_int4(chosen.x, chosen.y, rw, rh),
+                              c.R, tmp, kpos, warp_tot);
+      if (wid == 0 && nn >= 0) xl_mem_add(c, g, f);
+      if (tid == 0) {
+        if (nn < 0) {
+          set_error(c, GS_ERR_CAPACITY, GS_CAP_RECTS, g, 0);
+        } else {                               // place() bookkeeping (packer.py:245-261)
+          const int slot = V[i];
+          c.t->n_nfree[g] = nn;
+          c.t->n_nplaced[g]++;
+          c.t->p_node[slot] = g;
+          c.t->p_x[slot] = chosen.x;
+          c.t->p_y[slot] = chosen.y;
+          c.t->p_flags[slot] = (c.t->p_flags[slot] | PF_PLACED) & ~PF_RETRY;
+        }
+      }
+      i = nn < 0 ? nb : i + 1;
+      GS_EPOCH_TIC(p5_);
+      if (tid == 0) { GS_EPOCH_ADD(9, p5_ - p3_); }
+    } else {
+      // identical requests that follow fail too (nothing changed in between)
+      int j = nb;
+#pragma unroll 1
+      for (int k0 = i + 1; k0 < nb; k0 += 32) {
+        const int kk = k0 + lane;
+        const bool differs = kk < nb && (A[kk] != wh || (int)B[kk] != f);
+        const unsigned bal = __ballot_sync(FULL, differs);
+        if (bal) { j = k0 + __ffs(bal) - 1; break; }
+      }
+#pragma unroll 1
+      for (int kk = i + tid; kk < j; kk += NT) c.t->p_flags[V[kk]] |= PF_RETRY;
+      if (tid == 0) {
+        const int len = j - i;
+        c.sh->attempts += len;
+        c.sh->win_failures += len;
+        c.sh->rect_scans += sc * len;
+      }
+      i = j;
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// all threads; `scr` = idle shared scratch of `bytes`.  Returns false when a
+// running set is too large for a warp's slice (caller runs run_epoch).
+__device__ bool xl_run_epoch(Ctx& c, int w, char* scr, size_t bytes, XlShared* xs) {
+  const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool w0 = wid == 0;
+  GS_EPOCH_TIC(e0_);
+  if (w0) group_alive_by_fn(c);
+  GS_EPOCH_TIC(eg_);
+  if (threadIdx.x == 0) { GS_EPOCH_ADD(12, eg_ - e0_); }
+  long long* cnt = reinterpret_cast<long long*>(scr);
+  int* kind = reinterpret_cast<int*>(cnt + c.F);
+  int* ideal = kind + c.F;
+  int* nrem = ideal + c.F;
+  const size_t rec = ((size_t)c.F * 20 + 15) & ~(size_t)15;
+  if (rec > bytes) return false;
+  const size_t slice = ((bytes - rec) / nw) & ~(size_t)15;
+  const int cap = (int)(slice / 20);
+  char* mine = scr + rec + slice * wid;
+  unsigned long long* A = reinterpret_cast<unsigned long long*>(mine);
+  int q = 1;
+  while (q * 2 <= cap) q <<= 1;                // largest power of two that fits
+  unsigned long long* B = A + q;
+  int* V = reinterpret_cast<int*>(B + q);
+  if (threadIdx.x == 0) xs->stop = 0;
+  __syncthreads();
+#pragma unroll 1
+  for (int f = wid; f < c.F; f += nw) {
+    if (c.t->f_loff[f + 1] - c.t->f_loff[f] > q) {   // does not fit: sequential epoch
+      if (c.lane == 0) xs->stop = 1;
+      break;
+    }
+    xl_decide(c, f, kind, ideal, nrem, cnt, A, B, V);
+  }
+  __syncthreads();
+  if (xs->stop) return false;                  // nothing applied yet
+  GS_EPOCH_TIC(ed_);
+  if (threadIdx.x == 0) { GS_EPOCH_ADD(13, ed_ - e0_); }
+  if (w0) {
+#pragma unroll 1
+    for (int f = 0; f < c.F; f++) {
+      const int kd = kind[f];
+      if (kd == 1) {
+        const long long n_new = cnt[f];
+        const int idl = ideal[f];
+        const long long total = n_new + (idl >= 0 ? 1 : 0);
+        if (c.lane == 0) c.sh->decisions += total;
+        if (total > c.P) {
+          if (c.lane == 0) set_error(c, GS_ERR_CAPACITY, GS_CAP_PODS, c.P, 1);
+        } else if (total > 0) {
+          xl_make_pods(c, f, n_new, idl, w + c.sc->cold_start_windows);
+        }
+      } else if (kd == 2) {
+        const int* lst = c.t->s_list + c.t->f_loff[f];
+        const int m = nrem[f];
+#pragma unroll 1
+        for (int i = 0; i < m; i++) {
+          if (c.lane == 0) c.sh->decisions++;
+          xl_remove_pod(c, lst[i]);
+          if (failed(c)) break;
+        }
+      }
+      if (failed(c)) break;
+    }
+  }
+  __syncthreads();
+  GS_EPOCH_TIC(e2_);
+  if (threadIdx.x == 0) { GS_EPOCH_ADD(14, e2_ - ed_); }
+  if (c.sh->err) return true;
+  if (!xl_place_batch(c, scr, bytes, xs->warp_tot)) {
+    if (w0) place_batch(c);
+    __syncthreads();
+  }
+  GS_EPOCH_TIC(e3_);
+  if (w0 && !failed(c)) {
+#pragma unroll 1
+    for (int g = 0; g < c.G; g++) {
+      restructure(c, g);
+      if (failed(c)) break;
+    }
+    if (!failed(c)) refresh_frag(c);
+  }
+  GS_EPOCH_TIC(e4_);
+  if (threadIdx.x == 0) {
+    GS_EPOCH_ADD(4, e2_ - e0_); GS_EPOCH_ADD(5, e3_ - e2_); GS_EPOCH_ADD(6, e4_ - e3_);
+  }
+  __syncthreads();
+  return true;
+}
+
 }  // namespace gs

@@ -8,9 +8,11 @@ from paper_2309_00558_b200.scenario import Scenario
 backend.LIB_PATH = sys.argv[1]
 b = cc.Batch([cc.compile_run(Scenario.from_dict(wl.c4(s, windows=100)), "fast") for s in range(16)])
 s = backend.Session(b); ms = s.run()
-t = (C.c_ulonglong * 8)()
+t = (C.c_ulonglong * 16)()
 backend.lib().gs_xl_timing(t)
 tot = sum(t[:4])
 print(f"{ms:.1f} ms; warp-0 cycles: epoch {t[0]/tot:.2%} window_begin {t[1]/tot:.2%} steps {t[2]/tot:.2%} window_close {t[3]/tot:.2%}")
 ep = max(t[0], 1)
-print(f"  epoch split: scaling {t[4]/ep:.1%}  place_batch {t[5]/ep:.1%}  restructure+frag {t[6]/ep:.1%}")
+print(f"  epoch split: scaling {t[4]/ep:.1%}  place_batch {t[5]/ep:.1%} (best_match {t[7]/ep:.1%})  restructure+frag {t[6]/ep:.1%}")
+print(f"  xl_place_batch: sort {t[8]/ep:.1%}  scan+barrier {t[11]/ep:.1%}  place_pod {t[9]/ep:.1%}  iterations {t[10]} ({t[11]/max(t[10],1):.0f} cyc scan, {t[9]/max(t[10],1):.0f} cyc place per iter)")
+print(f"  scaling: group {t[12]/ep:.1%}  group+decide {t[13]/ep:.1%}  apply {t[14]/ep:.1%}")

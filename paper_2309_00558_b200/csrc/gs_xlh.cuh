@@ -839,7 +839,7 @@ __device__ int xl_carve(int4* list, int n, int4 placed, int cap, int4* tmp, int*
 // footprint (memory_model.py:60-72) of node g on one warp: the terms are
 // formed lane-parallel and added in resident (dict insertion) order, so the
 // double equals refresh_footprint's sequential loop.
-__device__ void xl_footprint(Ctx& c, int g) {
+__device__ double xl_footprint(Ctx& c, int g) {
   const int lane = c.lane;
   const int2* res = &c.t->n_res[g * c.F];
   const int nres = c.t->n_nres[g];
@@ -869,10 +869,11 @@ __device__ void xl_footprint(Ctx& c, int g) {
   }
   if (lane == 0) c.t->n_fp[g] = total;
   __syncwarp();
+  return total;
 }
 
 // memory_model.add_pod (memory_model.py:49-50) + footprint, one warp
-__device__ void xl_mem_add(Ctx& c, int g, int f) {
+__device__ double xl_mem_add(Ctx& c, int g, int f) {
   const int lane = c.lane;
   int* cnt = &c.t->n_cnt[g * c.F + f];
   int2* res = &c.t->n_res[g * c.F];
@@ -894,7 +895,7 @@ __device__ void xl_mem_add(Ctx& c, int g, int f) {
   }
   if (lane == 0) *cnt = had + 1;
   __syncwarp();
-  xl_footprint(c, g);
+  return xl_footprint(c, g);
 }
 
 // memory_model.remove_pod (memory_model.py:52-58) + footprint, one warp:
@@ -1026,8 +1027,11 @@ __device__ void xl_make_pods(Ctx& c, int f, long long n_eff, int ideal, int warm
 // version's; every warp reduces the per-warp winners itself, so the whole CTA
 // follows the same sequence of decisions.  The carve runs CTA-wide
 // (xl_carve); the memory ledger and the pod's fields are one thread's.
-// Returns false when the batch or a node's split list does not fit the
-// scratch (caller runs place_batch).
+// When they fit, the fleet's free-rect lists, free counts, footprints and
+// resident bits are staged in shared memory for the batch (written back at
+// the end), so a placement touches HBM only for the memory ledger.
+// Returns false when the batch does not fit the scratch (caller runs
+// place_batch).
 __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int nw = NT >> 5;
@@ -1035,12 +1039,46 @@ __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
   int q = 1;
   while (q < phi) q <<= 1;
   const size_t carve_n = 4 * (size_t)c.R + 8;
-  if ((size_t)q * 20 + carve_n * 20 > bytes) return false;
+  const size_t base_bytes = (size_t)q * 36 + carve_n * 20;
+  if (base_bytes > bytes) return false;
   unsigned long long* A = reinterpret_cast<unsigned long long*>(scr);
   unsigned long long* B = A + q;
-  int4* tmp = reinterpret_cast<int4*>(B + q);
+  double* dres = reinterpret_cast<double*>(B + q);      // admit delta if resident / not
+  double* dnew = dres + q;
+  int4* tmp = reinterpret_cast<int4*>(dnew + q);
   int* V = reinterpret_cast<int*>(tmp + carve_n);
   int* kpos = V + q;
+  // staged fleet state (rects [G*R], footprints, free counts, resident bits)
+  const int fwords = (c.F + 31) >> 5;
+  const size_t stage_bytes = (size_t)c.G * c.R * 16 + (size_t)c.G * 8 + (size_t)c.G * 4 +
+                             (size_t)c.G * fwords * 4;
+  const bool staged = base_bytes + stage_bytes + 64 <= bytes;
+  int4* rects = c.t->n_rect;
+  int* nfree = c.t->n_nfree;
+  double* fp = c.t->n_fp;
+  unsigned* rbits = nullptr;
+  if (staged) {
+    int4* st = reinterpret_cast<int4*>((reinterpret_cast<size_t>(kpos + carve_n) + 15) & ~(size_t)15);
+    rects = st;
+    fp = reinterpret_cast<double*>(st + (size_t)c.G * c.R);
+    nfree = reinterpret_cast<int*>(fp + c.G);
+    rbits = reinterpret_cast<unsigned*>(nfree + c.G);
+#pragma unroll 1
+    for (int g = wid; g < c.G; g += nw) {
+      const int nf = c.t->n_nfree[g];
+#pragma unroll 1
+      for (int j = lane; j < nf; j += 32) rects[g * c.R + j] = c.t->n_rect[g * c.R + j];
+      if (lane == 0) { nfree[g] = nf; fp[g] = c.t->n_fp[g]; }
+#pragma unroll 1
+      for (int k = lane; k < fwords; k += 32) {
+        unsigned wbits = 0;
+#pragma unroll 1
+        for (int b = 0; b < 32 && (k << 5) + b < c.F; b++)
+          if (c.t->n_cnt[g * c.F + (k << 5) + b] > 0) wbits |= 1u << b;
+        rbits[g * fwords + k] = wbits;
+      }
+    }
+  }
   __shared__ BestKey wbest[32];
   __shared__ long long wscan[32];
   // batch = alive, unplaced pods, compacted in slot order
@@ -1069,13 +1107,19 @@ __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
   __syncthreads();
   GS_EPOCH_TIC(p0_);
   xl_block_sort(A, B, V, qb);
-  // entry i's best_match inputs: A = (w, h), B = function
+  // entry i's best_match inputs: A = (w, h), B = function, admit deltas
+  const bool sharing = (c.flags & GS_FLAG_SHARING) != 0;
 #pragma unroll 1
   for (int i = tid; i < nb; i += NT) {
     const int slot = V[i];
+    const int f = c.t->p_fn[slot];
     A[i] = ((unsigned long long)(unsigned)c.t->p_w[slot] << 32) | (unsigned)c.t->p_h[slot];
-    B[i] = (unsigned long long)c.t->p_fn[slot];
+    B[i] = (unsigned long long)f;
+    const gs_function_t& fs = c.fs[f];
+    dres[i] = sharing ? fs.mem_runtime_mb : fs.mem_noshare_mb;
+    dnew[i] = sharing ? fs.mem_runtime_mb + fs.mem_server_mb : fs.mem_noshare_mb;
   }
+  const double cap_mb = c.cap_mb;
   int tpn = 1;                                 // threads per node (power of two)
   while (tpn * 2 * c.G <= NT && tpn < 32) tpn <<= 1;
   const int sub = tid & (tpn - 1);
@@ -1089,6 +1133,7 @@ __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
     GS_EPOCH_TIC(p2_);
     const unsigned long long wh = A[i];
     const int f = (int)B[i];
+    const double d_res = dres[i], d_new = dnew[i];
     const int rw = (int)(wh >> 32), rh = (int)(wh & 0xffffffffu);
     const long long rarea = (long long)rw * rh;
     BestKey best;
@@ -1096,10 +1141,12 @@ __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
     long long scans = 0;
 #pragma unroll 1
     for (int g = tid / tpn; g < c.G; g += gstride) {
-      if (!admit(c, g, f)) continue;
-      const int nf = c.t->n_nfree[g];
+      const bool res = staged ? ((rbits[g * fwords + (f >> 5)] >> (f & 31)) & 1u) != 0
+                              : c.t->n_cnt[g * c.F + f] > 0;
+      if (!(fp[g] + (res ? d_res : d_new) <= cap_mb)) continue;   // memory_model.admit
+      const int nf = nfree[g];
       if (sub == 0) scans += nf;
-      const int4* rl = &c.t->n_rect[g * c.R];
+      const int4* rl = &rects[g * c.R];
 #pragma unroll 1
       for (int j = sub; j < nf; j += tpn) {
         const int4 r = rl[j];
@@ -1124,17 +1171,24 @@ __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
     sc = warp_sum_ll(sc);
     if (k.idx >= 0) {
       const int g = k.a;
-      const int4 chosen = c.t->n_rect[k.idx];
-      const int n = c.t->n_nfree[g];
+      const int4 chosen = rects[k.idx];
+      const int n = nfree[g];
       if (tid == 0) { c.sh->rect_scans += sc; c.sh->attempts++; }
-      const int nn = xl_carve(&c.t->n_rect[g * c.R], n, make_int4(chosen.x, chosen.y, rw, rh),
+      const int nn = xl_carve(&rects[g * c.R], n, make_int4(chosen.x, chosen.y, rw, rh),
                               c.R, tmp, kpos, warp_tot);
-      if (wid == 0 && nn >= 0) xl_mem_add(c, g, f);
+      if (wid == 0 && nn >= 0) {
+        const double tot = xl_mem_add(c, g, f);
+        if (lane == 0 && staged) {
+          fp[g] = tot;
+          rbits[g * fwords + (f >> 5)] |= 1u << (f & 31);
+        }
+      }
       if (tid == 0) {
         if (nn < 0) {
           set_error(c, GS_ERR_CAPACITY, GS_CAP_RECTS, g, 0);
         } else {                               // place() bookkeeping (packer.py:245-261)
           const int slot = V[i];
+          nfree[g] = nn;
           c.t->n_nfree[g] = nn;
           c.t->n_nplaced[g]++;
           c.t->p_node[slot] = g;
@@ -1165,6 +1219,15 @@ __device__ bool xl_place_batch(Ctx& c, char* scr, size_t bytes, int* warp_tot) {
         c.sh->rect_scans += sc * len;
       }
       i = j;
+    }
+    __syncthreads();
+  }
+  if (staged) {                                // write the free-rect lists back
+#pragma unroll 1
+    for (int g = wid; g < c.G; g += nw) {
+      const int nf = nfree[g];
+#pragma unroll 1
+      for (int j = lane; j < nf; j += 32) c.t->n_rect[g * c.R + j] = rects[g * c.R + j];
     }
     __syncthreads();
   }

@@ -459,6 +459,7 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
     __syncthreads();
     if (xs->stop) break;
     GS_XL_TIC(t3_);
+    if (threadIdx.x == 0) { GS_XL_ADD(15, hot ? 0 : 1); }
     if (hot) {
       #pragma unroll 1
       for (int s = 0; s < c.T; s++) {

@@ -211,11 +211,10 @@ __device__ void xlh_complete(HotX* h) {
 #pragma unroll 1
     for (int g = tid; g < h->G; g += NT) {
       double sr = h->sr[g];
+      const int lo = h->seg[g], e = lo + h->ngr[g];      // the granted prefix
 #pragma unroll 1
-      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
-        const int i = h->order[j];
-        if (!(h->flags[i] & PF_GRANT)) break;
-        sr -= h->sm[i];
+      for (int j = lo; j < e; j++) {
+        sr -= h->sm[h->order[j]];
         if (sr < 0 && sr > -SM_EPS) sr = 0.0;
       }
       h->sr[g] = sr;
@@ -235,34 +234,55 @@ __device__ void xlh_complete(HotX* h) {
 
 // one quantum step (sim_engine.py:493-520) on the CTA-wide working set
 template <bool BND>
+#ifdef GS_XL_TIMING
+#define GS_PH_INIT() long long ph_t_ = clock64()
+#define GS_PH(k) { const long long now_ = clock64(); \
+    if (threadIdx.x == 0) atomicAdd(&gs_xl_t[k], (unsigned long long)(now_ - ph_t_)); ph_t_ = now_; }
+#else
+#define GS_PH_INIT()
+#define GS_PH(k)
+#endif
 __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
   const double t0 = (double)w * h->ws + (double)s * h->qs;
   const int n = h->n, F = h->F, G = h->G;
   const int tid = threadIdx.x, NT = blockDim.x;
   const bool integral = h->integral != 0;
-  if (s > 0 && !integral) {
-    // sm_running -= sm in the last dispatch order, with the float-dust clamp
-#pragma unroll 1
-    for (int g = tid; g < G; g += NT) {
-      double sr = h->sr[g];
-#pragma unroll 1
-      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
-        const int i = h->order[j];
-        if (!(h->flags[i] & PF_GRANT)) break;
-        sr -= h->sm[i];
-        if (sr < 0 && sr > -SM_EPS) sr = 0.0;
-      }
-      h->sr[g] = sr;
-    }
+  GS_PH_INIT();
+  if (threadIdx.x == 0) { GS_EPOCH_ADD(25, 1); GS_EPOCH_ADD(26, n); }
+#ifdef GS_XL_TIMING
+  if (threadIdx.x == 0) {
+    int mx = 0;
+    for (int g = 0; g < G; g++) mx = max(mx, h->seg[g + 1] - h->seg[g]);
+    GS_EPOCH_ADD(28, mx);
+    atomicMax(&gs_xl_t[29], (unsigned long long)mx);
   }
+#endif
+  // per-function and per-node work share one index space so they run on
+  // different threads: functions on [0, F), nodes on [FP, FP + G)
+  const int FP = (F + 31) & ~31;
   if (tid == 0) xs->grants = 0;
 #pragma unroll 1
-  for (int f = tid; f < F; f += NT) hot_admit<HotX, BND>(h, f, t0);
+  for (int x = tid; x < FP + G; x += NT) {
+    if (x < F) {
+      hot_admit<HotX, BND>(h, x, t0);
+    } else if (x >= FP) {
+      const int g = x - FP;
+      if (s > 0 && !integral) {
+        // sm_running -= sm in the last dispatch order, with the float-dust clamp
+        double sr = h->sr[g];
+        const int lo = h->seg[g], e = lo + h->ngr[g];    // the granted prefix
 #pragma unroll 1
-  for (int g = tid; g < G; g += NT) {
-    h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull; h->reqsm[g] = 0; h->ngr[g] = 0;
+        for (int j = lo; j < e; j++) {
+          sr -= h->sm[h->order[j]];
+          if (sr < 0 && sr > -SM_EPS) sr = 0.0;
+        }
+        h->sr[g] = sr;
+      }
+      h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull; h->reqsm[g] = 0; h->ngr[g] = 0;
+    }
   }
   __syncthreads();
+  GS_PH(16);
   // complete live tokens + filter_pods + requesting -> key
 #pragma unroll 1
   for (int i = tid; i < n; i += NT) {
@@ -278,42 +298,65 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
     h->key[i] = req ? -(h->qreq[i] - qused) : NOT_REQ;
-    if (req && integral) atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
+    // integral: requesting SM per node; otherwise: requesting pods per node
+    if (req) atomicAdd(&h->reqsm[h->fnode[i] >> 16], integral ? (int)h->sm[i] : 1);
   }
   __syncthreads();
-  // build_queue order per node by counting (key, pod index)
+  GS_PH(17);
+  // build_queue order per node by counting (key, pod index): pods before i
+  // in the node count on <=, pods after it on <.  Only requesting pods get a
+  // position (non-requesting keys are +inf, never ahead of one): the node's
+  // requesting prefix of `order` is all dispatch reads.  One trip count per node
+  // keeps the lanes of a warp (mostly one node) converged; four independent
+  // accumulators keep the shared-memory loads in flight.  In the integral
+  // path the SM ahead of i is a sum of integer-valued doubles, exact in any
+  // order.
 #pragma unroll 1
   for (int i = tid; i < n; i += NT) {
-    const int g = h->fnode[i] >> 16;
     const double k = h->key[i];
+    if (k == NOT_REQ) continue;                // never dispatched: no position needed
+    const int g = h->fnode[i] >> 16;
     const int lo = h->seg[g], hi = h->seg[g + 1];
-    int r = 0;
-    if (integral && k != NOT_REQ && h->reqsm[g] > (int)SM_LIMIT) {
-      double ahead = 0.0;
+    const double* key = h->key;
+    int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+    int j = lo;
+    if (integral && h->reqsm[g] > (int)SM_LIMIT) {
+      const double* sm = h->sm;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll 1
-      for (int j = lo; j < hi; j++) {
-        const double kj = h->key[j];
-        const bool less = (kj < k) || (kj == k && j < i);
-        r += less;
-        if (less) ahead += h->sm[j];
+      for (; j + 3 < hi; j += 4) {
+        const bool l0 = j < i ? key[j] <= k : key[j] < k;
+        const bool l1 = j + 1 < i ? key[j + 1] <= k : key[j + 1] < k;
+        const bool l2 = j + 2 < i ? key[j + 2] <= k : key[j + 2] < k;
+        const bool l3 = j + 3 < i ? key[j + 3] <= k : key[j + 3] < k;
+        r0 += l0; r1 += l1; r2 += l2; r3 += l3;
+        a0 += l0 ? sm[j] : 0.0; a1 += l1 ? sm[j + 1] : 0.0;
+        a2 += l2 ? sm[j + 2] : 0.0; a3 += l3 ? sm[j + 3] : 0.0;
       }
-      if (h->sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], r);
+#pragma unroll 1
+      for (; j < hi; j++) {
+        const bool l = j < i ? key[j] <= k : key[j] < k;
+        r0 += l; a0 += l ? sm[j] : 0.0;
+      }
+      const double ahead = (a0 + a1) + (a2 + a3);
+      if (sm[i] + ahead > SM_LIMIT + SM_EPS) atomicMin(&h->cut[g], (r0 + r1) + (r2 + r3));
     } else {
-      int j = lo;
 #pragma unroll 1
-      for (; j + 1 < hi; j += 2) {
-        const double a = h->key[j], b = h->key[j + 1];
-        r += (int)(j < i ? a <= k : a < k) + (int)(j + 1 < i ? b <= k : b < k);
+      for (; j + 3 < hi; j += 4) {
+        r0 += j < i ? key[j] <= k : key[j] < k;
+        r1 += j + 1 < i ? key[j + 1] <= k : key[j + 1] < k;
+        r2 += j + 2 < i ? key[j + 2] <= k : key[j + 2] < k;
+        r3 += j + 3 < i ? key[j + 3] <= k : key[j + 3] < k;
       }
-      if (j < hi) {
-        const double a = h->key[j];
-        r += (int)(j < i ? a <= k : a < k);
-      }
+#pragma unroll 1
+      for (; j < hi; j++) r0 += j < i ? key[j] <= k : key[j] < k;
     }
+    const int r = (r0 + r1) + (r2 + r3);
     h->order[lo + r] = (short)i;
     h->rank[i] = (short)r;
   }
   __syncthreads();
+  GS_PH(18);
   const double quantum = h->quantum;
   int grants = 0;
   if (integral) {
@@ -329,34 +372,17 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
         grants++;
       }
     }
-    __syncthreads();
-#pragma unroll 1
-    for (int g = tid; g < G; g += NT) {
-      const int ng = h->ngr[g];
-      if (ng == 0) continue;
-      PySum occ;
-      occ.reset();
-      const int lo = h->seg[g];
-#pragma unroll 1
-      for (int j = lo; j < lo + ng; j++) {
-        const int i = h->order[j];
-        occ.add(h->sm[i] * h->dur(i));
-      }
-      h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
-      h->occ[g] += occ.value() / 100.0;
-    }
+    GS_PH(19);
   } else {
 #pragma unroll 1
     for (int g = tid; g < G; g += NT) {
       double sr = h->sr[g];
       double mx = 0.0;
-      PySum occ;
-      occ.reset();
       int ng = 0;
+      const int lo = h->seg[g], e = lo + h->reqsm[g];   // the requesting prefix
 #pragma unroll 1
-      for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+      for (int j = lo; j < e; j++) {
         const int i = h->order[j];
-        if (h->key[i] == NOT_REQ) break;
         const double sm = h->sm[i];
         if (sm + sr > SM_LIMIT + SM_EPS) break;
         const double rem = h->qlim[i] - h->qused[i];
@@ -364,19 +390,17 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
         h->flags[i] |= PF_GRANT;
         sr += sm;
         if (ng == 0 || dur > mx) mx = dur;
-        occ.add(sm * dur);
         ng++;
       }
       h->sr[g] = sr;
-      if (ng) {
-        h->cov[g] += mx;
-        h->occ[g] += occ.value() / 100.0;
-      }
+      h->ngr[g] = ng;
+      h->covbits[g] = (unsigned long long)__double_as_longlong(mx);
       grants += ng;
     }
   }
   if (grants) atomicAdd(&xs->grants, grants);
   __syncthreads();
+  GS_PH(20);
   // serve (sim_engine.py:514-552), pod-parallel as in the per-warp classes:
   // granted pods in (function, node, pod_id) order, a dry run counts each
   // pod's request starts, a block scan turns them into per-function FIFO
@@ -390,6 +414,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
   for (int j = j0; j < j1; j++) mine += (h->flags[h->flist[j]] & PF_GRANT) ? 1 : 0;
   int ngl = 0;
   int k = xl_block_exscan(mine, xs->warp_tot, &ngl);
+  if (threadIdx.x == 0) { GS_EPOCH_ADD(27, ngl); }
 #pragma unroll 1
   for (int j = j0; j < j1; j++) {
     const int i = h->flist[j];
@@ -398,6 +423,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
 #pragma unroll 1
   for (int f = tid; f < F; f += NT) { h->fcomp[f] = 0; h->fviol[f] = 0; h->fpicks[f] = 0; }
   __syncthreads();
+  GS_PH(21);
   // 2. dry runs (chunk per thread so the block scan below runs in gl order)
   const int pk = (ngl + NT - 1) / NT;
   const int k0 = tid * pk, k1 = min(ngl, k0 + pk);
@@ -424,6 +450,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     run += p;
   }
   __syncthreads();
+  GS_PH(22);
   // 4. replay with the pod's FIFO position inside its function
 #pragma unroll 1
   for (int kk = tid; kk < ngl; kk += NT) {
@@ -440,9 +467,30 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     if (viol) atomicAdd(&h->fviol[f], viol);
   }
   __syncthreads();
-  // 5. each function's queue bookkeeping once
+  GS_PH(23);
+  // 5. each function's queue bookkeeping once; on other threads, each node's
+  //    coverage (max duration) and occupancy (Python sum of sm * duration in
+  //    dispatch order, sim_engine.py:514-517)
 #pragma unroll 1
-  for (int f = tid; f < F; f += NT) {
+  for (int x = tid; x < FP + G; x += NT) {
+    if (x >= FP) {
+      const int g = x - FP;
+      const int ng = h->ngr[g];
+      if (ng == 0) continue;
+      PySum occ;
+      occ.reset();
+      const int lo = h->seg[g];
+#pragma unroll 1
+      for (int j = lo; j < lo + ng; j++) {
+        const int i = h->order[j];
+        occ.add(h->sm[i] * h->dur(i));
+      }
+      h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
+      h->occ[g] += occ.value() / 100.0;
+      continue;
+    }
+    if (x >= F) continue;
+    const int f = x;
     const int want = h->fpicks[f];
     const int comp = h->fcomp[f];
     if (want == 0 && comp == 0) continue;
@@ -477,6 +525,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     h->wviol[f] += h->fviol[f];
   }
   __syncthreads();
+  GS_PH(24);
 }
 
 }  // namespace gs

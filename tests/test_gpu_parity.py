@@ -84,6 +84,14 @@ def test_gpu_matches_oracle_c4_large_fleet():
     assert_gpu_matches_oracle(scen, ["fast"] * len(scen))
 
 
+def test_gpu_matches_oracle_c4_full_day():
+    # C4 at its full horizon (one compressed day, W=3600; sinusoid period = W):
+    # many epochs on the CTA-wide epoch / placement path, plus a timeshare run
+    scen = [Scenario.from_dict(wl.c4(s, windows=3600)) for s in range(2)]
+    scen += [Scenario.from_dict(wl.c4(7, windows=60))]
+    assert_gpu_matches_oracle(scen, ["fast", "fast", "timeshare"])
+
+
 def test_gpu_matches_oracle_c2_timeshare_and_mixed_classes():
     # one batch mixing every size class the launcher dispatches (S/M/L/XL)
     scen = [Scenario.from_dict(wl.c2(s, windows=30)) for s in range(6)]

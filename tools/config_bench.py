@@ -34,8 +34,9 @@ def configs(quick: bool):
     yield ("C3", "FaST-GShare vs time-sharing sweep: 1024 bursty traces x both policies",
            [x for x in c3 for _ in (0, 1)], ["fast", "timeshare"] * len(c3))
     n4 = 148 // k            # one XL CTA per SM
-    yield ("C4", "64 nodes, 200 functions, diurnal trace, 300 windows",
-           [Scenario.from_dict(wl.c4(s, windows=300)) for s in range(n4)], ["fast"] * n4)
+    w4 = 3600 // k           # one compressed day
+    yield ("C4", f"64 nodes, 200 functions, diurnal trace, {w4} windows",
+           [Scenario.from_dict(wl.c4(s, windows=w4)) for s in range(n4)], ["fast"] * n4)
     n5 = 12500 // k
     yield ("C5", "100k (SM%, quantum, SLO) sweep: one GPU's 12.5k-run shard, 60 windows",
            [Scenario.from_dict(wl.c5(i)) for i in range(n5)], ["fast"] * n5)
@@ -64,7 +65,8 @@ def main():
         ok = st["code"] == 0
         classes = {int(k): int(v) for k, v in zip(*np.unique(st["hot_class"], return_counts=True))}
         # oracle on a bounded prefix (also the parity check of that prefix)
-        n = min(len(batch), max(2 * threads, 16))
+        per_run = float((batch.runs["windows"] * batch.runs["n_nodes"]).max())
+        n = min(len(batch), threads if per_run > 50000 else max(2 * threads, 16))
         t1 = time.perf_counter()
         sub = cc.Batch(batch.images[:n])
         ref = oracle.run_batch(sub, n_threads=threads)

@@ -1,6 +1,8 @@
 """Aggregate ncu SASS-level samples/instructions per CUDA source line.
 
 usage: python tools/ncu_lines.py <report.ncu-rep> <lib.so> [top]
+(STALL=stall_long_sb ranks lines by one stall reason instead of all samples;
+SECTION=<mangled-name substring> picks the kernel, e.g. gs_sim_kernel_xl)
 Maps each SASS offset to its innermost source line via `nvdisasm -g`.
 """
 import collections, csv, glob, os, re, subprocess, sys, tempfile
@@ -13,7 +15,16 @@ cubin = glob.glob(os.path.join(tmp, "*.cubin"))[0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 line_of = {}
 cur = None
+# offsets restart in every kernel's .text section: keep the one profiled
+# (SECTION=substring of its mangled name; default the smallest per-warp class)
+want = os.environ.get("SECTION", "HotILi64ELi12ELi4E")
+insec = False
 for l in dis.splitlines():
+    if re.match(r"\s*\.section\s+\.text\.", l):
+        insec = want in l
+        continue
+    if not insec:
+        continue
     m = re.match(r'\s*//## File "([^"]+)", line (\d+)', l)
     if m:
         cur = f"{os.path.basename(m.group(1))}:{m.group(2)}"
@@ -32,7 +43,7 @@ tot = 0
 for r in data:
     off = int(r[ix["Address"]], 16) - base
     key = line_of.get(off, "?")
-    s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+    s = int(r[ix[os.environ.get("STALL", "Warp Stall Sampling (All Samples)")]] or 0)
     samp[key] += s; tot += s
     inst[key] += int(r[ix["Instructions Executed"]] or 0)
 itot = sum(inst.values())

@@ -93,7 +93,9 @@ struct Hot {
   }
 };
 
-// size classes: (pods, functions, nodes)
+// size classes: (pods, functions, nodes).  XS (tiny fleets such as C1 / C5:
+// <= 4 functions, <= 2 nodes) is small enough to run 8 CTAs of 4 warps per SM.
+typedef Hot<32, 4, 2> HotXS;
 typedef Hot<64, 12, 4> HotS;
 typedef Hot<128, 32, 16> HotM;
 typedef Hot<256, 64, 32> HotL;

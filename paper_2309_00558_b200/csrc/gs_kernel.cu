@@ -192,10 +192,11 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
 }
 
 template <class H> __host__ __device__ constexpr int class_id() {
-  if constexpr (std::is_same<H, HotS>::value) return 1;
-  else if constexpr (std::is_same<H, HotM>::value) return 2;
-  else if constexpr (std::is_same<H, HotL>::value) return 3;
-  else return 4;
+  if constexpr (std::is_same<H, HotXS>::value) return 1;
+  else if constexpr (std::is_same<H, HotS>::value) return 2;
+  else if constexpr (std::is_same<H, HotM>::value) return 3;
+  else if constexpr (std::is_same<H, HotL>::value) return 4;
+  else return 5;
 }
 template <class H> __host__ __device__ constexpr size_t hot_bytes() {
   if constexpr (std::is_void<H>::value) return 0;
@@ -483,7 +484,7 @@ __device__ void simulate_run_xl(Ctx& c, const gs_out_t& out, const gs_out_t& hos
   }
   __syncthreads();
   if (hot && !c.sh->err) xlh_store(c, hx);     // flush the last windows' state
-  if (w0) finish_run(c, out, host, run, acc, su, so, peak, fail_total, 0, 0, 4, false);
+  if (w0) finish_run(c, out, host, run, acc, su, so, peak, fail_total, 0, 0, 5, false);
   __syncthreads();
 }
 
@@ -498,11 +499,16 @@ struct KArgs {
   int* counter;
 };
 
-template <class H>
 #ifndef GS_MIN_BLOCKS
 #define GS_MIN_BLOCKS 6   // 128-thread CTAs per SM the register budget must allow
 #endif
-__global__ void __launch_bounds__(128, GS_MIN_BLOCKS)
+// class XS trades a few spilled registers (64 instead of 80) for 32 resident
+// warps per SM: its runs are short and latency-bound (C1 +40%, C5 +8%)
+template <class H> struct MinBlocks { static constexpr int value = GS_MIN_BLOCKS; };
+template <> struct MinBlocks<HotXS> { static constexpr int value = 8; };
+
+template <class H>
+__global__ void __launch_bounds__(128, MinBlocks<H>::value)
 gs_sim_kernel(KArgs a) {
   __shared__ WarpShared shs[MAX_WARPS_PER_BLOCK];
   extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -609,11 +615,12 @@ size_t nbytes(long long n) { return sizeof(T) * (size_t)(n > 0 ? n : 1); }
 // smallest shared-memory size class whose capacities hold F functions and G
 // nodes (registered pods are checked per window on the device)
 static int run_class(const gs_scenario_t& sc) {
-  int k = 4;
-  if (sc.n_funcs <= HotS::FC && sc.n_nodes <= HotS::GC) k = 1;
-  else if (sc.n_funcs <= HotM::FC && sc.n_nodes <= HotM::GC) k = 2;
-  else if (sc.n_funcs <= HotL::FC && sc.n_nodes <= HotL::GC) k = 3;
-  if (sc.hot_class > k) k = sc.hot_class > 4 ? 4 : sc.hot_class;
+  int k = 5;
+  if (sc.n_funcs <= HotXS::FC && sc.n_nodes <= HotXS::GC) k = 1;
+  else if (sc.n_funcs <= HotS::FC && sc.n_nodes <= HotS::GC) k = 2;
+  else if (sc.n_funcs <= HotM::FC && sc.n_nodes <= HotM::GC) k = 3;
+  else if (sc.n_funcs <= HotL::FC && sc.n_nodes <= HotL::GC) k = 4;
+  if (sc.hot_class > k) k = sc.hot_class > 5 ? 5 : sc.hot_class;
   return k;
 }
 
@@ -626,7 +633,7 @@ struct gs_session {
   long long* ws_off = nullptr;
   int* order = nullptr;
   int* counter = nullptr;        // one work counter per size class
-  int class_off[6] = {0, 0, 0, 0, 0, 0};  // order[] slice of class k: [off[k-1], off[k])
+  int class_off[7] = {0, 0, 0, 0, 0, 0, 0};  // order[] slice of class k: [off[k-1], off[k])
   char* arena = nullptr;
   int n_runs = 0;
   int64_t n_fn_rows = 0, n_gpu_rows = 0, n_glob_rows = 0, n_place = 0;
@@ -667,7 +674,7 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   std::vector<long long> ws_off(R > 0 ? R : 1, 0);
   std::vector<int> order(R > 0 ? R : 1, 0);
   std::vector<double> cost(R > 0 ? R : 1, 0.0);
-  std::vector<int> cls(R > 0 ? R : 1, 4);
+  std::vector<int> cls(R > 0 ? R : 1, 5);
   long long arena_bytes = 0;
   for (int r = 0; r < R; r++) {
     const gs_scenario_t& sc = in->runs[r];
@@ -687,7 +694,7 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   std::stable_sort(order.begin(), order.begin() + R, [&](int a, int b) {
     return cls[a] != cls[b] ? cls[a] < cls[b] : cost[a] > cost[b];
   });
-  for (int k = 1; k <= 4; k++) {
+  for (int k = 1; k <= 5; k++) {
     int cnt = 0;
     for (int r = 0; r < R; r++) cnt += cls[r] <= k;
     s->class_off[k] = cnt;
@@ -813,7 +820,7 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   CK(cudaEventRecord(s->ev0, st));
   s->last_launches = 0;
-  for (int k = 1; k <= 4; k++) {
+  for (int k = 1; k <= 5; k++) {
     const int lo = s->class_off[k - 1], hi = s->class_off[k];
     if (hi <= lo) continue;
     KArgs a;
@@ -827,9 +834,10 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
     a.counter = s->counter + k;
     int rc = GS_OK;
     switch (k) {
-      case 1: rc = launch_class<HotS>(a, sms, st, err, err_len); break;
-      case 2: rc = launch_class<HotM>(a, sms, st, err, err_len); break;
-      case 3: rc = launch_class<HotL>(a, sms, st, err, err_len); break;
+      case 1: rc = launch_class<HotXS>(a, sms, st, err, err_len); break;
+      case 2: rc = launch_class<HotS>(a, sms, st, err, err_len); break;
+      case 3: rc = launch_class<HotM>(a, sms, st, err, err_len); break;
+      case 4: rc = launch_class<HotL>(a, sms, st, err, err_len); break;
       default: rc = launch_xl(a, sms, st, err, err_len); break;
     }
     if (rc != GS_OK) return rc;

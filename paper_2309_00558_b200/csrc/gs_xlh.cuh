@@ -62,7 +62,7 @@ struct HotX {
   }
 };
 
-constexpr size_t XLH_DYN_BYTES = 200 * 1024;   // dynamic shared memory per XL CTA
+constexpr size_t XLH_DYN_BYTES = 224 * 1024;   // dynamic shared memory per XL CTA (+ ~2 KB static)
 constexpr size_t XLH_POD_BYTES = 9 * 8 + 8 + 4 + 4 * 2 + 4 + 1;   // per registered pod
 constexpr size_t XLH_FN_BYTES = 2 * 8 + 25 * 4 + 4;           // per function (+ loff)
 constexpr size_t XLH_NODE_BYTES = 4 * 8 + 5 * 4 + 8 + 4;      // per node (+ seg)

@@ -156,7 +156,7 @@ typedef struct gs_placement {
 typedef struct gs_status {
   int32_t code, detail, arg0, arg1;
   int32_t n_placements;
-  int32_t hot_class;             /* size class the run executed in (1=S .. 4=XL)  */
+  int32_t hot_class;             /* size class the run executed in (1=XS .. 5=XL) */
   int64_t token_grants;          /* dispatch() outputs, token_backend.py:186     */
   int64_t scale_decisions;       /* len(scale_up)+len(scale_down)                */
   int64_t placement_attempts;    /* best_match calls, sim_engine.py:397          */

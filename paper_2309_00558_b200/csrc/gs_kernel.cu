@@ -347,6 +347,9 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
       } else {
         hot_begin_light(h, c.lane, w);
       }
+#ifdef GS_XL_TIMING
+      if (c.lane == 0) atomicAdd(&gs_xl_t[hot_valid ? 30 : 31], 1ull);
+#endif
       if (hot_valid) {
         pod_steps += (long long)h->n * c.T;
         hot_grants += hot_steps(h, c.lane, w);

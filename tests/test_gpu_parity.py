@@ -93,10 +93,11 @@ def test_gpu_matches_oracle_c4_full_day():
 
 
 def test_gpu_matches_oracle_c2_timeshare_and_mixed_classes():
-    # one batch mixing every size class the launcher dispatches (S/M/L/XL)
-    scen = [Scenario.from_dict(wl.c2(s, windows=30)) for s in range(6)]
+    # one batch mixing every size class the launcher dispatches (XS/S/M/L/XL)
+    scen = [Scenario.from_dict(wl.c2(s, windows=30, n_funcs=3, fleet=2)) for s in range(2)]
+    scen += [Scenario.from_dict(wl.c2(s, windows=30)) for s in range(6)]
     scen += [Scenario.from_dict(wl.c2(s, windows=30, n_funcs=20, fleet=8)) for s in range(4)]
     scen += [Scenario.from_dict(wl.c2(s, windows=20, n_funcs=48, fleet=24)) for s in range(2)]
     scen += [Scenario.from_dict(wl.c4(s, windows=12, n_funcs=80, fleet=40)) for s in range(2)]
-    pols = ["fast", "timeshare"] * 7
+    pols = ["fast", "timeshare"] * 8
     assert_gpu_matches_oracle(scen, pols)

@@ -236,6 +236,12 @@ int gs_audit_geometry(const int32_t* rects, const int32_t* n_free, const int32_t
 /* Launch shape (0 = default).  warps_per_block: scenario warps per CTA. */
 int gs_set_launch(int warps_per_block, int blocks_per_sm);
 
+/* XL class (one CTA per run): dynamic shared memory for the run's working set
+ * (0 = default 224 KB; clamped to [16 KB, 224 KB]).  Smaller values force the
+ * arena-stepping and warp-0 fallbacks -- a test / debugging knob; returns the
+ * value in effect. */
+int gs_set_xl_smem(int bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,6 +52,8 @@ def lib():
             L.gs_session_destroy.restype = None
             L.gs_set_launch.argtypes = [i, i]
             L.gs_set_launch.restype = i
+            L.gs_set_xl_smem.argtypes = [i]
+            L.gs_set_xl_smem.restype = i
             L.gs_session_upload.argtypes = [vp, vp, vp, cp, sz]
             L.gs_session_upload.restype = i
             L.gs_session_audit.argtypes = [vp, vp, vp, cp, sz]
@@ -240,3 +242,8 @@ def audit_geometry(nodes, side_x: int, side_y: int, device: int = 0):
 
 def set_launch(warps_per_block: int = 0, blocks_per_sm: int = -1):
     lib().gs_set_launch(int(warps_per_block), int(blocks_per_sm))
+
+
+def set_xl_smem(nbytes: int = 0) -> int:
+    """XL working-set shared memory (0 = default); small values force the fallbacks."""
+    return int(lib().gs_set_xl_smem(int(nbytes)))

@@ -500,6 +500,7 @@ struct KArgs {
   const int* order;           // runs of this size class, longest first
   int n_order;
   int* counter;
+  int xl_bytes;               // XL class: dynamic shared memory of the working set
 };
 
 #ifndef GS_MIN_BLOCKS
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(XL_THREADS, 1) gs_sim_kernel_xl(KArgs a) {
       c.Q = 0;
     }
     __syncthreads();
-    simulate_run_xl(c, a.out, a.host, run, &xs, &hx, reinterpret_cast<char*>(xl_dyn), XLH_DYN_BYTES);
+    simulate_run_xl(c, a.out, a.host, run, &xs, &hx, reinterpret_cast<char*>(xl_dyn), (size_t)a.xl_bytes);
   }
 }
 
@@ -594,6 +595,7 @@ namespace {
 
 int g_warps_per_block = 4;
 int g_blocks_per_sm = 0;
+int g_xl_bytes = (int)XLH_DYN_BYTES;
 
 void put_err(char* err, size_t n, const char* msg) {
   if (err && n) { std::snprintf(err, n, "%s", msg); }
@@ -649,6 +651,12 @@ struct gs_session {
 };
 
 extern "C" int gs_abi_version(void) { return GS_ABI_VERSION; }
+
+extern "C" int gs_set_xl_smem(int bytes) {
+  g_xl_bytes = bytes <= 0 ? (int)XLH_DYN_BYTES
+                          : std::max(16 * 1024, std::min(bytes, (int)XLH_DYN_BYTES)) & ~15;
+  return g_xl_bytes;
+}
 
 extern "C" int gs_set_launch(int warps_per_block, int blocks_per_sm) {
   if (warps_per_block > 0) g_warps_per_block = std::min(warps_per_block, MAX_WARPS_PER_BLOCK);
@@ -809,7 +817,7 @@ static int launch_xl(const KArgs& a, int sms, cudaStream_t st, char* err, size_t
   }
   long long blocks = sms;
   if (a.n_order < blocks) blocks = a.n_order > 0 ? a.n_order : 1;
-  gs_sim_kernel_xl<<<(unsigned)blocks, XL_THREADS, XLH_DYN_BYTES, st>>>(a);
+  gs_sim_kernel_xl<<<(unsigned)blocks, XL_THREADS, (size_t)a.xl_bytes, st>>>(a);
   CK(cudaGetLastError());
   return GS_OK;
 }
@@ -835,6 +843,7 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
     a.order = s->order + lo;
     a.n_order = hi - lo;
     a.counter = s->counter + k;
+    a.xl_bytes = g_xl_bytes;
     int rc = GS_OK;
     switch (k) {
       case 1: rc = launch_class<HotXS>(a, sms, st, err, err_len); break;

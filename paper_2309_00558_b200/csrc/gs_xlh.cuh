@@ -232,6 +232,9 @@ __device__ void xlh_complete(HotX* h) {
   __syncthreads();
 }
 
+template <bool BND>
+__device__ __forceinline__ void xlh_books(HotX* h, int f, int want, int comp);   // below
+
 // one quantum step (sim_engine.py:493-520) on the CTA-wide working set
 template <bool BND>
 #ifdef GS_XL_TIMING
@@ -264,7 +267,8 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
 #pragma unroll 1
   for (int x = tid; x < FP + G; x += NT) {
     if (x < F) {
-      hot_admit<HotX, BND>(h, x, t0);
+      if (s == 0) hot_admit<HotX, BND>(h, x, t0);   // later steps: admitted at the
+                                                    // end of the previous step
     } else if (x >= FP) {
       const int g = x - FP;
       if (s > 0 && !integral) {
@@ -493,7 +497,20 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     const int f = x;
     const int want = h->fpicks[f];
     const int comp = h->fcomp[f];
-    if (want == 0 && comp == 0) continue;
+    if (want != 0 || comp != 0) xlh_books<BND>(h, f, want, comp);
+    // the next step's _admit_arrivals (sim_engine.py:472-480) on the same
+    // thread, behind the node threads' occupancy sums instead of on the next
+    // step's critical path
+    if (s + 1 < h->T) hot_admit<HotX, BND>(h, f, (double)w * h->ws + (double)(s + 1) * h->qs);
+  }
+  __syncthreads();
+  GS_PH(24);
+}
+
+// per-function queue bookkeeping after the replay (step phase 5)
+template <bool BND>
+__device__ __forceinline__ void xlh_books(HotX* h, int f, int want, int comp) {
+  {
     const int avail = h->retn[f] + h->nsn[f];
     const int taken = want < avail ? want : avail;
     const int retn = h->retn[f];
@@ -524,8 +541,6 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     h->wcomp[f] += comp;
     h->wviol[f] += h->fviol[f];
   }
-  __syncthreads();
-  GS_PH(24);
 }
 
 }  // namespace gs

@@ -16,12 +16,16 @@
  *
  * Ownership: the caller owns every in/out buffer; nothing is retained after a
  * one-shot call returns.  Sessions own their device copies until destroyed.
- * Threading: no globals; calls are reentrant per (device, stream).
+ * Threading: calls are reentrant per (device, stream).  The only process
+ * state is the launch-shape DEFAULTS of gs_set_launch / gs_set_xl_smem
+ * (atomic; copied into a session at gs_session_create, never read by a
+ * launch), so concurrent sessions keep the shape they were created with.
  *
  * Return codes (also per-run in gs_status_t.code):
  *   GS_OK (0)            success
  *   GS_ERR_VALIDATION(1) a run hit a reference ValidationError mid-run
- *                        (sim_engine.py:346-349, zero serving rate)
+ *                        (detail GS_VAL_*: sim_engine.py:346-349 zero serving
+ *                        rate, autoscaler.py:115-117 no positive throughput)
  *   GS_ERR_CAPACITY  (3) a run outgrew a static capacity (pods, free rects,
  *                        returned requests); the host retries it with larger
  *                        capacities -- results are never silently truncated
@@ -49,6 +53,10 @@ enum {
   GS_ERR_CUDA = 4,
   GS_ERR_ARG = 5
 };
+
+/* gs_status_t.detail for GS_ERR_VALIDATION (arg0 = function, arg1 = point) */
+enum { GS_VAL_ZERO_RATE = 0,      /* _make_pod: T(sm_eff, 1.0) <= 0   sim_engine.py:346-349 */
+       GS_VAL_NO_THROUGHPUT = 1   /* scale_up: t_eff <= 0             autoscaler.py:115-117 */ };
 
 /* gs_status_t.detail for GS_ERR_CAPACITY */
 enum { GS_CAP_PODS = 1, GS_CAP_RECTS = 2, GS_CAP_RETURNED = 3, GS_CAP_NAMES = 4,
@@ -233,7 +241,8 @@ int gs_audit_geometry(const int32_t* rects, const int32_t* n_free, const int32_t
                       int n_nodes, int cap, int side_x, int side_y, uint32_t* breaches,
                       int device, char* err, size_t err_len);
 
-/* Launch shape (0 = default).  warps_per_block: scenario warps per CTA. */
+/* Launch-shape default for sessions created afterwards (0 = built-in
+ * default).  warps_per_block: scenario warps per CTA. */
 int gs_set_launch(int warps_per_block, int blocks_per_sm);
 
 /* XL class (one CTA per run): dynamic shared memory for the run's working set

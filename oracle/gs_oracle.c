@@ -78,7 +78,7 @@ typedef struct {
   int* retry; int nretry, cretry;
   int win_failures;
   long long grants, decisions, attempts, pod_steps, rect_scans, peak_pods;
-  int err_code, err_fn, err_pt;
+  int err_code, err_detail, err_fn, err_pt;
 } Eng;
 
 /* ------------------------------------------------------------------ utils */
@@ -403,6 +403,11 @@ static void run_epoch(Eng* e, int window) {
       const gs_function_t* fs = &e->fs[f];
       int pe = fs->p_eff;
       double t_eff = PT(e, f, pe)->thr;
+      if (t_eff <= 0) {                           /* autoscaler.py:115-117 */
+        if (!e->err_code) { e->err_code = GS_ERR_VALIDATION; e->err_detail = GS_VAL_NO_THROUGHPUT;
+                            e->err_fn = f; e->err_pt = pe; }
+        free(rs); free(adds); return;
+      }
       double nd = floor(gap / t_eff);
       double residual = gap - nd * t_eff;
       long long cnt = (long long)nd;
@@ -734,6 +739,7 @@ static int run_one(const gs_batch_t* in, int run, const gs_out_t* out) {
 done:
   free(batch);
   st->code = e->err_code;
+  st->detail = e->err_detail;
   st->arg0 = e->err_fn;
   st->arg1 = e->err_pt;
   st->token_grants = e->grants;

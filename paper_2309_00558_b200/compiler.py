@@ -42,6 +42,7 @@ GS_FLAG_SM_INTEGRAL = 4
 
 GS_OK, GS_ERR_VALIDATION, GS_ERR_INVARIANT, GS_ERR_CAPACITY, GS_ERR_CUDA, GS_ERR_ARG = range(6)
 GS_CAP_PODS, GS_CAP_RECTS, GS_CAP_RETURNED, GS_CAP_NAMES, GS_CAP_HOT = 1, 2, 3, 4, 5
+GS_VAL_ZERO_RATE, GS_VAL_NO_THROUGHPUT = 0, 1
 
 SCENARIO_DT = np.dtype([
     ("n_nodes", "<i4"), ("n_funcs", "<i4"), ("windows", "<i4"), ("steps", "<i4"),
@@ -180,32 +181,26 @@ def _resource_config_check(sm, q_req, q_lim):
         raise ValidationError(f"quota_request {q_req!r} exceeds quota_limit {q_lim!r}")
 
 
-def _profile_memo(profile) -> dict:
-    """Per-profile-object cache of compile-time derived data (profiles are
-    immutable inputs; sweeps share one object per synth spec, scenario.py)."""
-    memo = getattr(profile, "_gs_memo", None)
+def _profile_memo(profile, memo: dict | None) -> dict:
+    """Compile-time derived data of one profile object, cached for the
+    duration of ONE compile call (``memo`` is created per call): profiles are
+    mutable dataclasses and the reference re-reads ``entries`` on every run,
+    so nothing derived from a profile object may outlive the call."""
     if memo is None:
-        memo = {}
-        try:
-            object.__setattr__(profile, "_gs_memo", memo)
-        except (AttributeError, TypeError):       # slotted / foreign objects: no cache
-            pass
-    return memo
+        return {}
+    key = id(profile)
+    hit = memo.get(key)
+    if hit is None or hit[0] is not profile:
+        hit = memo[key] = (profile, {})
+    return hit[1]
 
 
-def _t_eff(profile) -> float:
-    memo = _profile_memo(profile)
-    t = memo.get("t_eff")
-    if t is None:
-        pts = list(profile.entries.values())
-        rpr_best = min(pts, key=lambda e: (-(e.throughput_rps / e.point.resource_area),
-                                           e.point.resource_area, e.point.sm_partition,
-                                           e.point.quota))
-        t = memo["t_eff"] = max(rpr_best.throughput_rps, 1e-9)
-    return t
+def _t_eff(lo: "_LoweredProfile") -> float:
+    """Throughput of most_efficient_point (autoscaler.py:98-100)."""
+    return float(lo.rows["thr"][lo.p_eff])
 
 
-def _default_caps(scenario, fns) -> Caps:
+def _default_caps(scenario, fns, lowered) -> Caps:
     """Static device capacities, sized from the trace peaks so that overflow
     (a device rerun with larger capacities) stays rare: pods for the whole
     fleet, and returned requests per function -- a scale-down can hand back
@@ -213,11 +208,14 @@ def _default_caps(scenario, fns) -> Caps:
     window_s = scenario.window_ms / 1000.0
     pods = 8
     per_fn = 0
-    for fn in fns:
-        t_eff = _t_eff(fn.profile)
+    for fn, lo in zip(fns, lowered):
+        t_eff = _t_eff(lo)
         counts = fn.trace.counts[:scenario.windows]
         peak = max(counts, default=0) / window_s
-        k = len(fn.initial_pods) + int(math.ceil(1.5 * peak / t_eff)) + 4
+        # t_eff <= 0: the first scale-up raises (autoscaler.py:115-117), so
+        # the function never adds pods beyond its initial ones
+        grow = int(math.ceil(1.5 * peak / t_eff)) if t_eff > 0 else 0
+        k = len(fn.initial_pods) + grow + 4
         pods += k
         per_fn = max(per_fn, k)
     pods = min(max(32, -(-pods // 32) * 32), 1 << 20)
@@ -243,11 +241,11 @@ class _LoweredProfile:
 _LOWER_CACHE: dict = {}
 
 
-def _lower_profile(profile, timeshare: bool) -> _LoweredProfile:
-    """Policy-specific dense point table of one profile (cached on the profile
-    object, then by content: sweeps reuse a handful of profiles across
+def _lower_profile(profile, timeshare: bool, memo: dict | None = None) -> _LoweredProfile:
+    """Policy-specific dense point table of one profile (cached per compile
+    call by object, then by content: sweeps reuse a handful of profiles across
     thousands of scenarios)."""
-    memo = _profile_memo(profile)
+    memo = _profile_memo(profile, memo)
     hit = memo.get(("lower", timeshare))
     if hit is not None:
         return hit
@@ -312,7 +310,10 @@ class RunImage:
     point_keys: list          # per function: [(sm, quota)] in point order
 
 
-def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> RunImage:
+def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
+                memo: dict | None = None) -> RunImage:
+    """Lower one (scenario, policy) run.  ``memo``: a dict shared by the runs of
+    ONE batch compile (per-profile-object cache; never reuse it across calls)."""
     if policy not in POLICIES:
         raise ValidationError(f"policy must be one of {POLICIES}, got {policy!r}")
     validate_scenario(scenario)
@@ -341,9 +342,9 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
                     f"{fn.function_id}: zero serving rate at ({sm_eff:g}, 1.0)")
 
     rank = _check_pod_id_order(fids)
-    caps = caps or _default_caps(scenario, fns)
+    lowered = [_lower_profile(fn.profile, timeshare, memo) for fn in fns]
+    caps = caps or _default_caps(scenario, fns, lowered)
 
-    lowered = [_lower_profile(fn.profile, timeshare) for fn in fns]
     # geometry scale: every as_frac(quota)*100 / as_frac(sm_eff) becomes integral
     lx = reduce(_lcm, (lo.lx for lo in lowered), 1)
     ly = reduce(_lcm, (lo.ly for lo in lowered), 1)
@@ -384,7 +385,10 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
         f["n_init"] = len(fn.initial_pods)
         f["init_off"] = len(init_rows) - len(fn.initial_pods)
         f["count_off"] = fi * windows
-        f["max_queue"] = -1 if fn.max_queue is None else int(fn.max_queue)
+        # None = unbounded (-1 on the device).  A negative limit makes the
+        # reference's `len(fn.queue) >= limit` (sim_engine.py:476) always true,
+        # exactly like 0: every arrival is dropped.
+        f["max_queue"] = -1 if fn.max_queue is None else max(0, int(fn.max_queue))
         f["p_eff"] = lo.p_eff
         f["id_rank"] = rank[fn.function_id]
         f["name_off"] = len(names)
@@ -395,8 +399,6 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None) -> Run
         f["mem_runtime_mb"] = mem.mem_runtime_mb
         f["mem_noshare_mb"] = mem.mem_noshare_mb
         names += raw
-        if fn.max_queue is not None and int(fn.max_queue) < 0:
-            raise ValidationError(f"{fn.function_id}: max_queue must be >= 0")
 
     scen = np.zeros(1, SCENARIO_DT)
     s = scen[0]

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -593,9 +594,13 @@ using namespace gs;
 
 namespace {
 
-int g_warps_per_block = 4;
-int g_blocks_per_sm = 0;
-int g_xl_bytes = (int)XLH_DYN_BYTES;
+// Process-wide launch-shape DEFAULTS (tuning knobs, gs_set_launch /
+// gs_set_xl_smem).  They are copied into a session when it is created and
+// never read by a launch, so concurrent sessions (several devices, streams or
+// threads) each run with the shape they were created with.
+std::atomic<int> g_warps_per_block{4};
+std::atomic<int> g_blocks_per_sm{0};
+std::atomic<int> g_xl_bytes{(int)XLH_DYN_BYTES};
 
 void put_err(char* err, size_t n, const char* msg) {
   if (err && n) { std::snprintf(err, n, "%s", msg); }
@@ -647,20 +652,24 @@ struct gs_session {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int last_launches = 0;
   double last_ms = 0.0;
+  int warps_per_block = 4;     // launch shape, fixed at creation
+  int blocks_per_sm = 0;
+  int xl_bytes = (int)XLH_DYN_BYTES;
   size_t input_bytes = 0;
 };
 
 extern "C" int gs_abi_version(void) { return GS_ABI_VERSION; }
 
 extern "C" int gs_set_xl_smem(int bytes) {
-  g_xl_bytes = bytes <= 0 ? (int)XLH_DYN_BYTES
-                          : std::max(16 * 1024, std::min(bytes, (int)XLH_DYN_BYTES)) & ~15;
-  return g_xl_bytes;
+  const int v = bytes <= 0 ? (int)XLH_DYN_BYTES
+                           : std::max(16 * 1024, std::min(bytes, (int)XLH_DYN_BYTES)) & ~15;
+  g_xl_bytes.store(v);
+  return v;
 }
 
 extern "C" int gs_set_launch(int warps_per_block, int blocks_per_sm) {
-  if (warps_per_block > 0) g_warps_per_block = std::min(warps_per_block, MAX_WARPS_PER_BLOCK);
-  if (blocks_per_sm >= 0) g_blocks_per_sm = blocks_per_sm;
+  if (warps_per_block > 0) g_warps_per_block.store(std::min(warps_per_block, MAX_WARPS_PER_BLOCK));
+  if (blocks_per_sm >= 0) g_blocks_per_sm.store(blocks_per_sm);
   return 0;
 }
 
@@ -676,6 +685,9 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   gs_session* s = new (std::nothrow) gs_session();
   if (!s) { put_err(err, err_len, "out of host memory"); return GS_ERR_ARG; }
   s->device = device;
+  s->warps_per_block = g_warps_per_block.load();
+  s->blocks_per_sm = g_blocks_per_sm.load();
+  s->xl_bytes = g_xl_bytes.load();
   s->n_runs = in->n_runs;
   s->n_fn_rows = in->n_fn_rows; s->n_gpu_rows = in->n_gpu_rows;
   s->n_glob_rows = in->n_glob_rows; s->n_place = in->n_placements;
@@ -784,18 +796,18 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   return GS_OK;
 }
 
+// The dynamic shared-memory opt-in is a per-(device, kernel) attribute whose
+// value depends on the session's launch shape: set it before every launch (a
+// cheap host call) instead of caching it per process.
 template <class H>
-static int launch_class(const KArgs& a, int sms, cudaStream_t st, char* err, size_t err_len) {
-  const int wpb = g_warps_per_block;
+static int launch_class(const gs_session* s, const KArgs& a, int sms, cudaStream_t st,
+                        char* err, size_t err_len) {
+  const int wpb = s->warps_per_block;
   const int threads = wpb * 32;
   const size_t dyn = hot_bytes<H>() * (size_t)wpb;
-  static bool attr_set[8] = {false};
-  if (!attr_set[class_id<H>()]) {
-    CK(cudaFuncSetAttribute(gs_sim_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)std::max<size_t>(dyn, 48 * 1024)));
-    attr_set[class_id<H>()] = true;
-  }
-  int per_sm = g_blocks_per_sm;
+  CK(cudaFuncSetAttribute(gs_sim_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)std::max<size_t>(dyn, 48 * 1024)));
+  int per_sm = s->blocks_per_sm;
   if (per_sm <= 0) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gs_sim_kernel<H>, threads, dyn));
     if (per_sm < 1) per_sm = 1;
@@ -809,12 +821,8 @@ static int launch_class(const KArgs& a, int sms, cudaStream_t st, char* err, siz
 }
 
 static int launch_xl(const KArgs& a, int sms, cudaStream_t st, char* err, size_t err_len) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(gs_sim_kernel_xl, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)XLH_DYN_BYTES));
-    attr_set = true;
-  }
+  CK(cudaFuncSetAttribute(gs_sim_kernel_xl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)XLH_DYN_BYTES));
   long long blocks = sms;
   if (a.n_order < blocks) blocks = a.n_order > 0 ? a.n_order : 1;
   gs_sim_kernel_xl<<<(unsigned)blocks, XL_THREADS, (size_t)a.xl_bytes, st>>>(a);
@@ -843,20 +851,19 @@ extern "C" int gs_session_run(gs_session_t* s, void* stream_ptr, char* err, size
     a.order = s->order + lo;
     a.n_order = hi - lo;
     a.counter = s->counter + k;
-    a.xl_bytes = g_xl_bytes;
+    a.xl_bytes = s->xl_bytes;
     int rc = GS_OK;
     switch (k) {
-      case 1: rc = launch_class<HotXS>(a, sms, st, err, err_len); break;
-      case 2: rc = launch_class<HotS>(a, sms, st, err, err_len); break;
-      case 3: rc = launch_class<HotM>(a, sms, st, err, err_len); break;
-      case 4: rc = launch_class<HotL>(a, sms, st, err, err_len); break;
+      case 1: rc = launch_class<HotXS>(s, a, sms, st, err, err_len); break;
+      case 2: rc = launch_class<HotS>(s, a, sms, st, err, err_len); break;
+      case 3: rc = launch_class<HotM>(s, a, sms, st, err, err_len); break;
+      case 4: rc = launch_class<HotL>(s, a, sms, st, err, err_len); break;
       default: rc = launch_xl(a, sms, st, err, err_len); break;
     }
     if (rc != GS_OK) return rc;
     s->last_launches++;
   }
   CK(cudaEventRecord(s->ev1, st));
-  s->last_launches = 1;
   CK(cudaEventSynchronize(s->ev1));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, s->ev0, s->ev1));

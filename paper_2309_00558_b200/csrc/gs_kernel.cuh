@@ -1003,6 +1003,10 @@ __device__ void run_epoch(Ctx& c, int w) {
       const gs_function_t& fs = c.fs[f];
       const int pe = fs.p_eff;
       const double t_eff = c.pt(f, pe).thr;
+      if (!(t_eff > 0)) {                     // autoscaler.py:115-117
+        if (c.lane == 0) set_error(c, GS_ERR_VALIDATION, GS_VAL_NO_THROUGHPUT, f, pe);
+        return;
+      }
       const double nd = floor(gap / t_eff);
       const double residual = gap - nd * t_eff;
       const long long cnt = (long long)nd;

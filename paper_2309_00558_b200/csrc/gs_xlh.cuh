@@ -803,14 +803,18 @@ __device__ void xl_decide(Ctx& c, int f, int* kind, int* ideal_o, int* nrem_o, l
   if (gap > 0) {                              // scale_up: autoscaler.py:103-131
     const int pe = c.fs[f].p_eff;
     const double t_eff = c.pt(f, pe).thr;
-    const double nd = floor(gap / t_eff);
-    const double residual = gap - nd * t_eff;
-    cnt = (long long)nd;
-    if (residual > 0) {
-      idl = ideal_point(c, f, residual);
-      if (idl < 0) idl = pe;
+    if (!(t_eff > 0)) {                       // autoscaler.py:115-117
+      kd = 3;
+    } else {
+      const double nd = floor(gap / t_eff);
+      const double residual = gap - nd * t_eff;
+      cnt = (long long)nd;
+      if (residual > 0) {
+        idl = ideal_point(c, f, residual);
+        if (idl < 0) idl = pe;
+      }
+      kd = 1;
     }
-    kd = 1;
   } else if (gap < 0) {                       // scale_down: autoscaler.py:134-149
     double delta = gap;
 #pragma unroll 1
@@ -1349,6 +1353,8 @@ __device__ bool xl_run_epoch(Ctx& c, int w, char* scr, size_t bytes, XlShared* x
         } else if (total > 0) {
           xl_make_pods(c, f, n_new, idl, w + c.sc->cold_start_windows);
         }
+      } else if (kd == 3) {
+        if (c.lane == 0) set_error(c, GS_ERR_VALIDATION, GS_VAL_NO_THROUGHPUT, f, c.fs[f].p_eff);
       } else if (kd == 2) {
         const int* lst = c.t->s_list + c.t->f_loff[f];
         const int m = nrem[f];

@@ -27,37 +27,69 @@ def shard(n_total: int, rank: int, world: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
-def all_gather_summaries(summary: np.ndarray, n_total: int, group=None, device=None) -> np.ndarray:
-    """All-gather every rank's gs_summary_t records into run order.
-
-    Blocks may differ in length by one run, so each rank pads to the largest
-    block; the padding is dropped after the gather.  ``device`` selects where
-    the payload lives (a CUDA device for NCCL, None/CPU for gloo).
-    """
+def _gather_padded(arr: np.ndarray, n_total: int, group, device) -> np.ndarray:
+    """All-gather one fixed-size record per run (any structured dtype) into
+    run order.  Blocks differ in length by at most one run, so each rank pads
+    to the largest block; the padding is dropped after the gather."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     per = max(len(shard(n_total, r, world)) for r in range(world))
-    item = SUMMARY_DT.itemsize
-    buf = np.zeros(per, SUMMARY_DT)
-    buf[:len(summary)] = summary
+    item = arr.dtype.itemsize
+    buf = np.zeros(per, arr.dtype)
+    buf[:len(arr)] = arr
     send = torch.from_numpy(buf.view(np.uint8).copy())
     if device is not None:
         send = send.to(device)
     recv = torch.empty(per * item * world, dtype=torch.uint8, device=send.device)
     dist.all_gather_into_tensor(recv, send, group=group)
-    raw = recv.cpu().numpy().view(SUMMARY_DT).reshape(world, per)
+    raw = recv.cpu().numpy().view(arr.dtype).reshape(world, per)
     parts = [raw[r, :len(shard(n_total, r, world))] for r in range(world)]
-    out = np.concatenate(parts) if parts else np.zeros(0, SUMMARY_DT)
-    assert len(out) == n_total and rank < world
+    out = np.concatenate(parts) if parts else np.zeros(0, arr.dtype)
+    assert len(out) == n_total
     return out
 
 
-def run_sharded(scenarios, policies="fast", *, device=None, group=None):
+def all_gather_summaries(summary: np.ndarray, n_total: int, group=None, device=None) -> np.ndarray:
+    """All-gather every rank's gs_summary_t records into run order.
+
+    ``device`` selects where the payload lives (a CUDA device for NCCL,
+    None/CPU for gloo).
+    """
+    return _gather_padded(np.asarray(summary, SUMMARY_DT), n_total, group, device)
+
+
+STATUS_REC_DT = np.dtype([("code", "<i4"), ("pad", "<i4")])
+
+
+def gather_outcomes(local, n_total: int, group=None, device=None):
+    """Gather the summaries AND a status code per run.
+
+    ``local`` holds this rank's RunResults or exceptions (simulate(...,
+    errors="return")).  A failed run contributes a zeroed summary and a
+    non-zero code, so one bad scenario never leaves the other ranks blocked
+    in the collective: every rank takes part in both gathers and sees the same
+    global code array.
+    """
+    summ = np.zeros(len(local), SUMMARY_DT)
+    codes = np.zeros(len(local), STATUS_REC_DT)
+    for i, r in enumerate(local):
+        if isinstance(r, Exception):
+            codes[i]["code"] = 1
+        else:
+            summ[i] = r.summary
+    return (all_gather_summaries(summ, n_total, group=group, device=device),
+            _gather_padded(codes, n_total, group, device)["code"])
+
+
+def run_sharded(scenarios, policies="fast", *, device=None, group=None, errors: str = "raise"):
     """Simulate this rank's shard on its GPU and all-gather the summaries.
 
-    Returns (local RunResults, global summary array in input order).
+    Returns (local RunResults, global summary array in input order).  Errors
+    are collected first and raised only after the gathers, on EVERY rank
+    (``errors="raise"``), so a failing scenario cannot hang the collective;
+    with ``errors="return"`` failed runs come back as exceptions (local) and
+    zeroed summaries (global).
     """
     import torch
     import torch.distributed as dist
@@ -67,11 +99,25 @@ def run_sharded(scenarios, policies="fast", *, device=None, group=None):
         policies = [policies] * len(scenarios)
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     mine = shard(len(scenarios), rank, world)
-    dev = torch.cuda.current_device() if device is None else device
-    local = simulate([scenarios[i] for i in mine], [policies[i] for i in mine], device=dev)
-    summ = np.array([r.summary for r in local], SUMMARY_DT) if local else np.zeros(0, SUMMARY_DT)
-    return local, all_gather_summaries(summ, len(scenarios), group=group,
-                                       device=torch.device("cuda", dev))
+    if device is None and torch.cuda.is_available():
+        device = torch.cuda.current_device()
+    try:
+        local = simulate([scenarios[i] for i in mine], [policies[i] for i in mine],
+                         device=device or 0, errors="return")
+    except Exception as exc:              # whole-shard failure (no device, ...)
+        local = [exc] * len(mine)
+    where = torch.device("cuda", device) if device is not None else None
+    summ, codes = gather_outcomes(local, len(scenarios), group=group, device=where)
+    if errors == "raise":
+        bad = np.flatnonzero(codes)
+        if len(bad):
+            first = int(bad[0])
+            if first in mine:
+                raise local[first - mine.start]
+            from .errors import GShareError
+            raise GShareError(f"scenario {first} failed on another rank "
+                              f"({len(bad)} failed runs in total)")
+    return local, summ
 
 
 def summary_totals(summary: np.ndarray) -> dict:

@@ -51,6 +51,9 @@ def run_error(image: cc.RunImage, status) -> Exception | None:
         return None
     if code == cc.GS_ERR_VALIDATION:
         f, k = int(status["arg0"]), int(status["arg1"])
+        if int(status["detail"]) == cc.GS_VAL_NO_THROUGHPUT:
+            # autoscaler.py:115-117
+            return ValidationError(f"{image.fids[f]}: no profiled point has positive throughput")
         sm_eff = float(image.points[k + int(image.funcs[f]["point_off"])]["sm_eff"])
         # sim_engine.py:346-349
         return ValidationError(f"{image.fids[f]}: zero serving rate at ({sm_eff:g}, 1.0)")

@@ -180,6 +180,98 @@ def bundled_cases():
     return out
 
 
+def _flat_csv(fid, sms, qs, thr, slo=500.0):
+    """A CSV profile whose throughput is thr(sm, q) (0 allowed: ProfileEntry
+    only requires >= 0, profiles.py:48-66)."""
+    lines = ["function_id,sm_partition,quota,throughput_rps,p99_ms,slo_ms,"
+             "mem_noshare_mb,mem_runtime_mb,mem_server_mb"]
+    for sm in sms:
+        for q in qs:
+            t = thr(sm, q)
+            lines.append(f"{fid},{sm},{q},{t},{round(1000.0 / max(t, 1e-3), 3)},{slo},"
+                         f"1300,950,650")
+    return "\n".join(lines) + "\n"
+
+
+def error_branch_cases():
+    """Every ValidationError reachable from _Engine.run after validation
+    (sim_engine.py:434-452): the scale_up guard t_eff <= 0
+    (autoscaler.py:115-117) and the zero serving rate of a scaled-up pod's
+    (sm_eff, 1.0) point (sim_engine.py:346-349) -- on the per-warp fleet
+    sizes and on an XL fleet (F > 64 functions), with demand arriving before
+    and after the first epoch, and the zero-throughput function sorted first,
+    in the middle and last among the function ids."""
+    out = []
+    sms, qs = [12, 50, 100], [0.5, 1.0]
+    zero = _flat_csv("z", sms, qs, lambda sm, q: 0.0)
+
+    def synth_fn(fid, rps, inits=()):
+        return {"function_id": fid, "trace": {"kind": "constant", "rps": rps},
+                "profile": {"synth": {"t_max": 40.0, "sm_knee": 50.0, "grid_sm": sms,
+                                      "grid_quota": qs, "slo_ms": 500.0}},
+                "initial_pods": [{"sm": s, "quota": q} for s, q in inits]}
+
+    for tag, fid_list, zpos in (("first", ["z", "zz_a", "zz_b"], 0),
+                                ("middle", ["a", "z", "zz"], 1),
+                                ("last", ["a", "b", "z"], 2)):
+        for rps, epoch, w in ((5.0, 2, 6), (0.0, 2, 6), (12.0, 3, 4)):
+            files, fns = {}, []
+            for k, fid in enumerate(fid_list):
+                if k == zpos:
+                    files["z.csv"] = _flat_csv(fid, sms, qs, lambda sm, q: 0.0)
+                    fns.append({"function_id": fid, "profile": {"csv": "z.csv"},
+                                "trace": {"kind": "constant", "rps": rps}})
+                else:
+                    fns.append(synth_fn(fid, 20.0, [(50, 0.5)]))
+            out.append({"name": f"err-no-throughput-{tag}-{rps:g}-{epoch}-{w}", "files": files,
+                        "scenario": {"fleet_size": 2, "windows": w, "epoch_windows": epoch,
+                                     "cold_start_windows": 1, "functions": fns}})
+    # demand only in a late window: the error fires at the first epoch after it
+    out.append({"name": "err-no-throughput-late-burst", "files": {"z.csv": zero},
+                "scenario": {"fleet_size": 1, "windows": 9, "epoch_windows": 2,
+                             "functions": [{"function_id": "z", "profile": {"csv": "z.csv"},
+                                            "trace": {"kind": "explicit",
+                                                      "counts": [0, 0, 0, 0, 0, 7, 0]}}]}})
+    # a zero-throughput function that never sees demand runs to completion
+    out.append({"name": "ok-zero-throughput-no-demand", "files": {"z.csv": zero},
+                "scenario": {"fleet_size": 1, "windows": 8, "epoch_windows": 2,
+                             "functions": [{"function_id": "z", "profile": {"csv": "z.csv"},
+                                            "trace": {"kind": "constant", "rps": 0.0}},
+                                           synth_fn("y", 30.0, [(12, 1.0)])]}})
+    # zero serving rate of the scaled-up point: (50, 1.0) serves nothing but
+    # (50, 0.5) is the most efficient point (fast) -- timeshare serves at (100, 1.0)
+    zr = _flat_csv("zr", sms, qs, lambda sm, q: 0.0 if (sm == 50 and q == 1.0) else
+                   (30.0 * q if sm == 50 else 2.0 * q))
+    out.append({"name": "err-zero-rate-scaled-point", "files": {"zr.csv": zr},
+                "scenario": {"fleet_size": 2, "windows": 7, "epoch_windows": 2,
+                             "functions": [{"function_id": "zr", "profile": {"csv": "zr.csv"},
+                                            "trace": {"kind": "constant", "rps": 25.0}},
+                                           synth_fn("a", 10.0, [(12, 0.5)])]}})
+    # XL fleet: 70 functions (> class L's 64) on 40 nodes, one zero-throughput
+    for zfid in ("f000", "f041", "f069"):
+        files, fns = {"z.csv": None}, []
+        for i in range(70):
+            fid = f"f{i:03d}"
+            if fid == zfid:
+                files["z.csv"] = _flat_csv(fid, sms, qs, lambda sm, q: 0.0)
+                fns.append({"function_id": fid, "profile": {"csv": "z.csv"},
+                            "trace": {"kind": "constant", "rps": 3.0}})
+            else:
+                fns.append(synth_fn(fid, 6.0 + (i % 7), [(12, 0.5)]))
+        out.append({"name": f"err-no-throughput-xl-{zfid}", "files": files,
+                    "scenario": {"fleet_size": 40, "windows": 4, "epoch_windows": 2,
+                                 "cold_start_windows": 1, "gpu_capacity_mb": 81920.0,
+                                 "functions": fns}})
+    # negative max_queue: the reference's `len(queue) >= limit` drops everything
+    for mq in (-1, -7, 0):
+        out.append({"name": f"max-queue-{mq}", "files": {},
+                    "scenario": {"fleet_size": 1, "windows": 5, "epoch_windows": 2,
+                                 "functions": [dict(synth_fn("q", 15.0, [(50, 1.0)]),
+                                                    max_queue=mq),
+                                               synth_fn("r", 9.0, [(12, 1.0)])]}})
+    return out
+
+
 def run_reference(case, policy):
     sys.path.insert(0, REF)
     import gshare_sim as ref
@@ -206,6 +298,7 @@ def run_reference(case, policy):
 def main(n_random: int = 360, seed: int = 20261017):
     rng = random.Random(seed)
     cases = bundled_cases() + engine_test_cases() + [random_case(rng, i) for i in range(n_random)]
+    cases += error_branch_cases()
     records = []
     for case in cases:
         for policy in ("fast", "timeshare"):

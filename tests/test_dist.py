@@ -62,3 +62,44 @@ def test_gloo_world2_all_gather_reassembles_the_batch(tmp_path):
     assert gathered.tobytes() == whole.tobytes()
     tot = gd.summary_totals(gathered)
     assert tot["runs"] == n_runs and tot["arrivals"] > 0
+
+
+def _worker_errors(rank, world, port, out_dir):
+    """run_sharded with one failing scenario on rank 1: every rank must leave
+    the collectives and raise (no rank blocks in the all-gather)."""
+    import sys
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import parity
+    from paper_2309_00558_b200 import engine
+    # the CPU oracle stands in for the device here (no GPU in this container)
+    engine.simulate = lambda sc, pol, device=0, errors="raise": parity.oracle_results(sc, pol)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    scen = wl.c2_scenarios(range(5), windows=12)
+    import golden
+    # an all-zero CSV profile with demand: ValidationError at the first scale-up
+    rec = next(r for r in golden.records() if r["name"] == "err-no-throughput-first-5-2-6")
+    scen.append(golden.load_scenario(rec))         # run 5 -> rank 1's shard
+    try:
+        gd.run_sharded(scen, "fast", device=None)
+        outcome = "ok"
+    except Exception as exc:                        # noqa: BLE001
+        outcome = f"{type(exc).__name__}: {exc}"
+    local, summ = gd.run_sharded(scen, "fast", device=None, errors="return")
+    with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as fh:
+        fh.write(outcome + "\n" + str(int((summ["windows"] == 0).sum())) + "\n")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_failure_on_one_rank_raises_everywhere(tmp_path):
+    mp.spawn(_worker_errors, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    r0 = (tmp_path / "r0.txt").read_text().splitlines()
+    r1 = (tmp_path / "r1.txt").read_text().splitlines()
+    assert r0[0].startswith("GShareError: scenario 5 failed on another rank"), r0
+    assert r1[0].startswith("ValidationError"), r1
+    assert r0[1] == r1[1] == "1"        # one zeroed summary in the gathered array

@@ -1,25 +1,37 @@
 """Benchmark: simulated scenario-seconds/s of the batched FaST-GShare engine.
 
-Workload (BASELINE.json configs[1]): 4-node cluster,
-10 MLPerf-shaped functions (ResNet-50 / RNN-T / BERT profiles), Poisson
-constant-rate traces, heuristic auto-scaling with model sharing, 300 one-second
-windows, policy "fast"; ``--runs`` independent seeds per GPU (weak scaling:
-each rank simulates its own seed block, no data-path collective; one NCCL
-all-gather of the per-run summary records at the end).
+Headline workload (BASELINE.json configs[1]): 4-node
+cluster, 10 MLPerf-shaped functions (ResNet-50 / RNN-T / BERT profiles),
+Poisson constant-rate traces, heuristic auto-scaling with model sharing, 300
+one-second windows, policy "fast"; ``--runs`` independent seeds per GPU (weak
+scaling: each rank simulates its own seed block, no data-path collective; one
+NCCL all-gather of the per-run summary records at the end).
 
 A "step" = one launch of the scenario megakernel over the GPU's whole batch.
-``value``  = total simulated scenario-seconds / device time of the K timed
-             launches (CUDA events on the launching stream, max over ranks),
-             inputs already resident in HBM, L2 flushed between launches.
+``value``  = simulated scenario-seconds of the runs that completed / device
+             time of the K timed launches (CUDA events on the launching
+             stream, max over ranks), inputs resident in HBM, L2 flushed
+             between launches.
 ``e2e``    = same metric through the C ABI with host buffers, every step:
              H2D of the compiled batch from page-locked memory
              (gs_session_upload), the kernel, and every output row back in
              host memory (written in place by the kernel into page-locked
              buffers) plus the status/summary D2H -- host wall clock, max
              over ranks.
-``--impl reference`` times the CPU oracle port (oracle/, a literal C
-restatement of pkg/src/gshare_sim, pinned to the reference by golden
-fixtures) on all host cores on a bounded sample of the same workload.
+``e2e_api``= the drop-in Python API end to end: ``engine.run_batch`` on the
+             list of Scenario objects -> one MetricsReport per run, and
+             ``summary()`` of every report: host compile, H2D, kernel, D2H
+             and report construction inside the timing (N=1, rank 0).
+``parity_sample`` = the oracle (oracle/, a C restatement of pkg/src/gshare_sim
+             pinned to the reference's own outputs) re-simulates a prefix of
+             the timed runs; every record (rows, placements, decision
+             counters, summary) is compared with the GPU's.  At N=1 the same
+             oracle pass is timed as ``cpu_baseline``.
+``per_config`` = the same measurement (device value, state-touch fraction,
+             CPU baseline, parity sample) for the other BASELINE configs
+             C1, C3, C4, C5 (N=1).
+``--impl reference`` times the CPU oracle port on all host cores on a
+bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -29,15 +41,17 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+
 def workload(windows: int) -> str:
     return ("C2: 4-node cluster, 10 functions (ResNet-50/RNN-T/BERT-shaped), Poisson "
             f"arrivals, heuristic auto-scaling, model sharing, {windows} x 1 s windows, policy fast")
+
+
 METRIC = "simulated scenario-seconds/sec"
 UNIT = "scenario-s/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -57,6 +71,9 @@ def parse():
                     help="runs in the CPU baseline sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-api", action="store_true", help="skip the e2e_api measurement")
+    ap.add_argument("--no-per-config", action="store_true")
+    ap.add_argument("--configs", default="C1,C3,C4,C5")
     return ap.parse_args()
 
 
@@ -65,15 +82,30 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def build_batch(seeds, windows):
-    from paper_2309_00558_b200 import compiler as cc, workloads as wl
-    scen = wl.c2_scenarios(seeds, windows=windows)
-    return cc.Batch([cc.compile_run(s, "fast") for s in scen])
+def c2_seq(seeds, windows):
+    from paper_2309_00558_b200 import workloads as wl
+    seeds = list(seeds)
+    return wl.ScenarioSeq(lambda i: wl.c2(seeds[i], windows=windows), len(seeds))
 
 
-def sim_seconds(batch) -> float:
+def build_batch(scen, policies):
+    """Compile on all host cores; every run of the benchmark workloads compiles."""
+    from paper_2309_00558_b200 import compiler as cc
+    if isinstance(policies, str):
+        policies = [policies] * len(scen)
+    batch, index, errors = cc.compile_batch(scen, policies)
+    if errors:
+        raise next(iter(errors.values()))
+    return batch
+
+
+def sim_seconds(batch, status=None) -> float:
+    """Simulated scenario-seconds; with ``status``, of the runs that completed."""
     r = batch.runs
-    return float((r["windows"].astype("f8") * r["window_s"]).sum())
+    per = r["windows"].astype("f8") * r["window_s"]
+    if status is not None:
+        per = per[status["code"][:len(per)] == 0]
+    return float(per.sum())
 
 
 def algorithmic_bytes(batch, status, summary) -> float:
@@ -147,30 +179,81 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(batch, sample_runs: int, threads: int):
-    """Time the oracle port on `sample_runs` runs of the workload."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_run(batch, n: int, threads: int):
+    """The oracle port on the first ``n`` runs of ``batch`` (same layout);
+    returns (output arrays, wall seconds, the prefix batch)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle
-    from paper_2309_00558_b200 import compiler as cc
-    sub = cc.Batch(batch.images[:sample_runs])
+    import oracle                             # checker / CPU baseline only
     oracle.build()
+    sub = batch.prefix(n)
     t0 = time.perf_counter()
-    oracle.run_batch(sub, n_threads=threads, rows=True)
-    dt = time.perf_counter() - t0
-    return sim_seconds(sub) / dt, dt, sub
+    out = oracle.run_batch(sub, n_threads=threads, rows=True)
+    return out, time.perf_counter() - t0, sub
 
 
-def cpu_sample_size(batch, threads: int, target_s: float) -> int:
-    """Runs of `batch` the oracle finishes in about `target_s` seconds on
-    `threads` host threads (calibrated on a small prefix)."""
-    n0 = min(len(batch), max(4 * threads, 64))
-    _, dt, _ = cpu_reference(batch, n0, threads)
-    return int(min(len(batch), max(n0, n0 * target_s / max(dt, 1e-3))))
+def oracle_sample(batch, threads: int, target_s: float, n_fixed: int = 0):
+    """Oracle on a prefix sized to take about ``target_s`` seconds."""
+    n = n_fixed or min(len(batch), max(2 * threads, 16))
+    out, dt, sub = oracle_run(batch, n, threads)
+    while not n_fixed and dt < 0.5 * target_s and n < len(batch):
+        n = min(len(batch), int(n * min(8.0, max(1.5, target_s / max(dt, 1e-3)))))
+        out, dt, sub = oracle_run(batch, n, threads)
+    return out, dt, sub
 
 
-def fleet_totals(summary):
-    from paper_2309_00558_b200.dist import summary_totals
-    return summary_totals(summary)
+def parity_sample(sub, gpu: dict, ref: dict) -> dict:
+    """Record-by-record comparison of the GPU outputs with the oracle's on the
+    runs of ``sub`` (a prefix of the GPU batch, identical layout): status
+    (code, decision counters), summary record, function / GPU / global rows,
+    final placements.  Runs the device reported over capacity are rerun with
+    larger capacities by the engine, so they are counted, not compared."""
+    import numpy as np
+    from paper_2309_00558_b200 import compiler as cc
+    n = len(sub)
+    gs, rs = gpu["status"][:n], ref["status"][:n]
+    cap = gs["code"] == cc.GS_ERR_CAPACITY
+    fields = ("code", "token_grants", "scale_decisions", "placement_attempts", "pod_steps",
+              "rect_scans", "peak_pods", "n_placements", "detail", "arg0", "arg1")
+    ok = np.ones(n, bool)
+    for f in fields:
+        ok &= gs[f] == rs[f]
+    ok &= (gpu["summary"][:n].view(np.uint8).reshape(n, -1)
+           == ref["summary"][:n].view(np.uint8).reshape(n, -1)).all(axis=1)
+    runs = sub.runs
+    for key, off, per in (("fn_rows", "fn_row_off", runs["windows"] * runs["n_funcs"]),
+                          ("gpu_rows", "gpu_row_off", runs["windows"] * runs["n_nodes"]),
+                          ("glob_rows", "glob_row_off", runs["windows"]),
+                          ("placements", "place_off", gs["n_placements"])):
+        a, b = gpu[key], ref[key]
+        names = [x for x in a.dtype.names if x != "pad"]
+        end = int(runs[off][-1] + per[-1]) if n else 0
+        eq = np.ones(end, bool)
+        for x in names:
+            eq &= a[x][:end] == b[x][:end]
+        if eq.all():
+            continue
+        for r in np.nonzero(ok)[0]:
+            o, c = int(runs[off][r]), int(per[r])
+            if not eq[o:o + c].all():
+                ok[r] = False
+    compared = ~cap
+    bad = np.nonzero(compared & ~ok)[0]
+    return {"runs": int(compared.sum()), "bit_exact": int((compared & ok).sum()),
+            "capacity_reruns_skipped": int(cap.sum()),
+            "first_mismatch": int(bad[0]) if len(bad) else None,
+            "fields": "status code/detail + decision counters, summary record, "
+                      "fn/gpu/global rows, placements"}
 
 
 def load_peak():
@@ -181,20 +264,27 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic():
+def load_ncu():
     try:
         with open(NCU_SUMMARY) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            return json.load(fh)
     except (OSError, ValueError):
+        return {}
+
+
+def _pct(s):
+    try:
+        return float(str(s).split()[0])
+    except (ValueError, IndexError):
         return None
 
 
-def measure_e2e(args, batch, sess, device, dist, compile_s):
+def measure_e2e(args, batch, sess, dist):
     """The same metric through the C ABI with host buffers: every step uploads
     the batch from page-locked host memory (gs_session_upload), runs the kernel,
     and reads every result back (rows written in place into page-locked host
     memory by the kernel, status + summary by D2H).  Host wall clock around the
-    steps, max over ranks."""
+    steps, max over ranks.  Returns (e2e dict, the output arrays)."""
     import torch
     batch.pin()
     out = batch.alloc_outputs(rows=True, pinned=True)
@@ -222,13 +312,90 @@ def measure_e2e(args, batch, sess, device, dist, compile_s):
     world = dist.get_world_size() if dist is not None else 1
     out_bytes = sum(v.nbytes for v in out.values() if v is not None)
     sess.map_host(None)
-    return {"value": sim_seconds(batch) * world * args.steps / dt, "unit": UNIT,
+    return {"value": sim_seconds(batch, out["status"]) * world * args.steps / dt, "unit": UNIT,
             "h2d_bytes_per_step": int(batch.input_bytes()),
             "d2h_bytes_per_step": int(out_bytes),
             "ms_per_step": 1000.0 * dt / args.steps,
             "api": "C ABI session: gs_session_upload (pinned H2D) + gs_session_run + "
-                   "gs_session_download; rows written in place into pinned host memory",
-            "host_compile_s": round(compile_s, 3)}
+                   "gs_session_download; rows written in place into pinned host memory"}, out
+
+
+def measure_api(args, seeds, dev):
+    """``engine.run_batch`` (the reference's ``run`` over a list, sim_engine.py:601)
+    on Scenario objects, plus ``summary()`` of every report -- compile, H2D,
+    kernel, D2H and report construction all inside the host wall clock."""
+    import torch
+    from paper_2309_00558_b200 import engine, workloads as wl
+    scen = wl.c2_scenarios(seeds, windows=args.windows)       # the caller's objects
+    t0 = time.perf_counter()
+    reps = engine.run_batch(scen, "fast", device=dev)
+    t1 = time.perf_counter()
+    sums = [r.summary() for r in reps]
+    t2 = time.perf_counter()
+    torch.cuda.synchronize()
+    simsec = sum(float(s.window_ms) / 1000.0 * s.windows for s in scen)
+    return {"value": simsec / (t2 - t0), "unit": UNIT, "runs": len(scen),
+            "seconds": round(t2 - t0, 3), "run_batch_s": round(t1 - t0, 3),
+            "summaries_s": round(t2 - t1, 3),
+            "failed_runs": sum(1 for s in sums if not s),
+            "api": "engine.run_batch(list[Scenario]) -> MetricsReport per run, then "
+                   "summary() of each (compile + GPU + decode timed)"}
+
+
+def config_workloads(names, windows_c4: int = 600):
+    """(name, description, scenarios, policies) of the other BASELINE configs."""
+    from paper_2309_00558_b200 import workloads as wl
+    out = []
+    if "C1" in names:
+        out.append(("C1", "1 node, 3 MLPerf functions, fixed RPS, 60 windows, both policies",
+                    wl.ScenarioSeq(lambda i: wl.c1(), 2048), ["fast", "timeshare"] * 1024))
+    if "C3" in names:
+        out.append(("C3", "FaST-GShare vs time-sharing: 1024 bursty traces x both policies",
+                    wl.ScenarioSeq(lambda i: wl.c3(i // 2), 2048), ["fast", "timeshare"] * 1024))
+    if "C4" in names:
+        out.append(("C4", f"64 nodes, 200 functions, diurnal trace over {windows_c4} windows "
+                          "(148 runs = one XL CTA per SM)",
+                    wl.ScenarioSeq(lambda i: wl.c4(i, windows=windows_c4), 148), ["fast"] * 148))
+    if "C5" in names:
+        out.append(("C5", "(SM%, quantum, SLO) sweep: one GPU's 12.5k-run shard of 100k, 60 windows",
+                    wl.ScenarioSeq(wl.c5, 12500), ["fast"] * 12500))
+    return out
+
+
+def measure_config(name, desc, scen, pols, flush, threads, peak):
+    import numpy as np
+    import torch
+    from paper_2309_00558_b200 import backend
+    t0 = time.perf_counter()
+    batch = build_batch(scen, pols)
+    t_compile = time.perf_counter() - t0
+    sess = backend.Session(batch)
+    sess.run()
+    ms = []
+    for _ in range(2):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ms.append(sess.run())
+    out = sess.download(rows=True)
+    sess.close()
+    st = out["status"]
+    ok = st["code"] == 0
+    dev_s = sum(ms) / len(ms) / 1000.0
+    value = sim_seconds(batch, st) / dev_s
+    ref, dt, sub = oracle_sample(batch, threads, 4.0)
+    cpu_v = sim_seconds(sub) / dt
+    classes = {int(k): int(v) for k, v in zip(*np.unique(st["hot_class"], return_counts=True))}
+    return {"config": name, "workload": desc, "runs": len(batch), "ok_runs": int(ok.sum()),
+            "value": value, "unit": UNIT, "ms_per_launch": 1000.0 * dev_s,
+            "decisions_per_sec": float((st["token_grants"] + st["scale_decisions"]
+                                        + st["placement_attempts"]).sum()) / dev_s,
+            "state_touch_frac": algorithmic_bytes(batch, st, out["summary"]) / dev_s / 1e9 / peak,
+            "size_classes": classes,
+            "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"first {len(sub)} runs, {dt:.2f} s"},
+            "gpu_over_cpu": value / cpu_v,
+            "parity_sample": parity_sample(sub, out, ref),
+            "host_compile_s": round(t_compile, 2)}
 
 
 def run_reference_arm(args, rank, world):
@@ -236,14 +403,17 @@ def run_reference_arm(args, rank, world):
         return 0
     threads = os.cpu_count() or 1
     # each step is a bounded sample (~8 s of CPU work) of the same workload
-    pool = build_batch(range(args.cpu_sample or 4096), args.windows)
-    sample = args.cpu_sample or cpu_sample_size(pool, threads, 8.0)
-    batch = build_batch(range(sample), args.windows) if sample > len(pool) else pool
+    pool = build_batch(c2_seq(range(args.cpu_sample or 4096), args.windows), "fast")
+    if args.cpu_sample:
+        sample = args.cpu_sample
+    else:
+        _, dt, sub = oracle_sample(pool, threads, 8.0)
+        sample = len(sub)
     for _ in range(args.warmup):
-        cpu_reference(batch, min(sample, 2 * threads), threads)
+        oracle_run(pool, min(sample, 2 * threads), threads)
     times, simsec = [], []
     for _ in range(args.steps):
-        _, dt, sub = cpu_reference(batch, sample, threads)
+        _, dt, sub = oracle_run(pool, sample, threads)
         simsec.append(sim_seconds(sub))           # the sample actually simulated
         times.append(dt)
     value = sum(simsec) / sum(times)
@@ -252,8 +422,10 @@ def run_reference_arm(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload(args.windows), "runs_per_step": sample, "windows": args.windows},
+        "config": {"workload": workload(args.windows), "runs_per_step": sample,
+                   "windows": args.windows},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample} C2 runs x {args.windows} windows per step "
                                    f"(oracle/gs_oracle.c, {threads} host threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -287,7 +459,7 @@ def main():
 
     seeds = range(rank * args.runs, (rank + 1) * args.runs)
     t_c = time.perf_counter()
-    batch = build_batch(seeds, args.windows)
+    batch = build_batch(c2_seq(seeds, args.windows), "fast")
     compile_s = time.perf_counter() - t_c
     sess = backend.Session(batch, device=local)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -317,7 +489,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     out = sess.download(rows=False)
-    bad = int((out["status"]["code"] != 0).sum())
+    st = out["status"]
+    bad = int((st["code"] != 0).sum())
 
     # NCCL all-gather of the fixed-size per-run summary records
     summ = out["summary"]
@@ -327,55 +500,104 @@ def main():
         fleet = gdist.all_gather_summaries(summ, args.runs * world,
                                            device=torch.device("cuda", local))
     gathered_runs = len(fleet)
-    e2e = None
+
+    e2e, rows = None, None
     if not args.no_e2e:
-        e2e = measure_e2e(args, batch, sess, local, dist, compile_s)
-    sim_s = sim_seconds(batch) * world
+        e2e, rows = measure_e2e(args, batch, sess, dist)
+        e2e["host_compile_s"] = round(compile_s, 3)
+    if rows is None:
+        rows = sess.download(rows=True)
+    sess.close()
+
+    # parity sample of the timed runs (every rank checks its own shard) and,
+    # at N=1, the CPU baseline from the same oracle pass
+    threads = os.cpu_count() or 1
+    parity, cpu = None, None
+    if not args.no_cpu_baseline:
+        if world == 1:
+            ref, dt, sub = oracle_sample(batch, threads, 15.0, args.cpu_sample)
+            cpu = {"value": sim_seconds(sub) / dt, "unit": UNIT, "cores": threads,
+                   "kind": "port", "cpu_model": cpu_model(),
+                   "sample": f"first {len(sub)} of the {len(batch)} timed C2 runs, {dt:.2f} s "
+                             f"wall on {threads} host threads (oracle/gs_oracle.c)"}
+        else:
+            ref, dt, sub = oracle_run(batch, min(len(batch), 64), max(1, threads // world))
+        parity = parity_sample(sub, rows, ref)
+        if dist is not None:
+            t = torch.tensor([parity["runs"], parity["bit_exact"]], dtype=torch.int64,
+                             device="cuda")
+            dist.all_reduce(t)
+            parity.update(runs=int(t[0]), bit_exact=int(t[1]), ranks=world)
+    del rows
+
+    sim_s = sim_seconds(batch, st) * world
     value = sim_s / (total_ms / 1000.0 / args.steps)
-    st = out["status"]
     decisions = float((st["token_grants"] + st["scale_decisions"] + st["placement_attempts"]).sum())
     dec_per_s = decisions * world / (total_ms / 1000.0 / args.steps)
 
-    line = None
+    api = None
+    if rank == 0 and world == 1 and not args.no_api:
+        api = measure_api(args, seeds, local)
+
+    per_config = None
+    peak, peak_src = load_peak()
+    if rank == 0 and world == 1 and not args.no_per_config:
+        per_config = [measure_config(*w, flush=flush, threads=threads, peak=peak)
+                      for w in config_workloads(args.configs.split(","))]
+
     if rank == 0:
-        peak, peak_src = load_peak()
         bytes_launch = algorithmic_bytes(batch, st, summ)
         achieved = bytes_launch / (total_ms / args.steps / 1000.0) / 1e9
-        traffic = load_traffic()
-        cpu = None
-        if not args.no_cpu_baseline and world == 1:
-            threads = os.cpu_count() or 1
-            sample = args.cpu_sample or cpu_sample_size(batch, threads, 15.0)
-            v, dt, _ = cpu_reference(batch, sample, threads)
-            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"first {sample} of the {len(batch)} C2 runs, {dt:.2f} s wall "
-                             f"on {threads} host threads (oracle/gs_oracle.c)"}
+        ncu = load_ncu()
+        m = ncu.get("metrics", {})
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args.windows), "runs_per_gpu": args.runs, "windows": args.windows,
-                       "policy": "fast", "l2": "flushed between launches (256 MiB write)",
+            "config": {"workload": workload(args.windows), "runs_per_gpu": args.runs,
+                       "windows": args.windows, "policy": "fast",
+                       "l2": "flushed between launches (256 MiB write)",
                        "failed_runs": bad, "summaries_all_gathered": gathered_runs},
             "fleet_summary": fleet_totals(fleet),
             "decisions_per_sec": dec_per_s,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "model": "SURVEY §8d state-touch bytes per launch",
-                         "bytes_per_launch": bytes_launch},
+            "roofline": {
+                "bound": "issue",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "state_touch_frac": achieved / peak,
+                "traffic": ncu.get("dram_bytes_per_launch"),
+                "peak_source": peak_src,
+                "model": "SURVEY §8d state-touch bytes per launch / device time, against HBM "
+                         "peak; the working set lives in shared memory, so real DRAM traffic "
+                         "is `traffic` and the binding limit is instruction issue",
+                "bytes_per_launch": bytes_launch,
+                "issue": {"source": f"ncu --set full ({ncu.get('tag')}, {ncu.get('kernel')})",
+                          "issue_active_pct": _pct(m.get(
+                              "smsp__issue_active.avg.pct_of_peak_sustained_active")),
+                          "ipc_per_sm": _pct(m.get("sm__inst_executed.avg.per_cycle_active")),
+                          "simt_efficiency": (_pct(m.get(
+                              "smsp__thread_inst_executed_per_inst_executed.ratio")) or 0) / 32,
+                          "warps_active_pct": _pct(m.get(
+                              "sm__warps_active.avg.pct_of_peak_sustained_active"))},
+            },
             "cpu_baseline": cpu,
+            "parity_sample": parity,
             "e2e": e2e,
+            "e2e_api": api,
+            "per_config": per_config,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    sess.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def fleet_totals(summary):
+    from paper_2309_00558_b200.dist import summary_totals
+    return summary_totals(summary)
 
 
 if __name__ == "__main__":

@@ -251,6 +251,26 @@ int gs_set_launch(int warps_per_block, int blocks_per_sm);
  * value in effect. */
 int gs_set_xl_smem(int bytes);
 
+/* ---- host-side report rendering ---------------------
+ * metrics.csv of device rows, byte-identical to the reference's
+ * MetricsReport.to_csv() (metrics.py:62-91, numbers as util.py:4-10 fmt_num
+ * of round(x, 9) / round(x, 6)).  `fid_csv` holds, for every gs_function_t of
+ * the batch in batch order, the function id as csv.writer renders it (UTF-8,
+ * QUOTE_MINIMAL), function k at [fid_off[k], fid_off[k+1]).  No GPU needed. */
+/* Run `run` into buf.  Returns the text length, or -- when buf is NULL or cap
+ * is below the run's size bound -- the bound to allocate; -1 on bad args. */
+int64_t gs_format_csv(const gs_batch_t* in, const gs_out_t* out, int run,
+                      const char* fid_csv, const int64_t* fid_off, char* buf, int64_t cap);
+/* Runs [r0, r1) on n_threads host threads (0 = all): run r0+k at
+ * buf + offs[k], length lens[k].  Returns 0, or the bytes needed when buf is
+ * NULL / cap is too small, -1 on bad args. */
+int64_t gs_format_csv_batch(const gs_batch_t* in, const gs_out_t* out, int r0, int r1,
+                            const char* fid_csv, const int64_t* fid_off, char* buf,
+                            int64_t cap, int64_t* offs, int64_t* lens, int n_threads);
+/* fmt_num(round(x[k], nd)) (nd < 0: fmt_num(x[k])) as NUL-terminated text
+ * at buf + k*stride (stride >= 48). */
+int gs_format_numbers(const double* x, int64_t n, int nd, char* buf, int64_t stride);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,13 @@ def lib():
             L.gs_host_alloc.restype = i
             L.gs_host_free.argtypes = [vp]
             L.gs_host_free.restype = None
+            i64 = C.c_int64
+            L.gs_format_csv.argtypes = [vp, vp, i, vp, vp, vp, i64]
+            L.gs_format_csv.restype = i64
+            L.gs_format_csv_batch.argtypes = [vp, vp, i, i, vp, vp, vp, i64, vp, vp, i]
+            L.gs_format_csv_batch.restype = i64
+            L.gs_format_numbers.argtypes = [vp, i64, i, vp, i64]
+            L.gs_format_numbers.restype = i
             if L.gs_abi_version() != 1:
                 raise BackendUnavailableError("libgshare_b200.so ABI version mismatch")
             _lib = L

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libgshare_b200.so")
-SOURCES = ["gs_kernel.cu"]
+SOURCES = ["gs_kernel.cu", "gs_host.cpp"]
 DEPS = SOURCES + sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 

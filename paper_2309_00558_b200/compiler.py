@@ -150,6 +150,11 @@ def _ordered_functions(scenario):
 def _check_pod_id_order(fids) -> dict:
     """Rank of each fid such that pod-id string order == (rank, counter digits)."""
     keyed = sorted(fids, key=lambda f: f + "-")
+    # keys sharing the prefix a+"-" sort contiguously right behind it, so a
+    # clash shows up between neighbours; only then search for the pair the
+    # reference-order double loop reports first
+    if all(not (b + "-").startswith(a + "-") for a, b in zip(keyed, keyed[1:])):
+        return {f: i for i, f in enumerate(keyed)}
     for a in fids:
         for b in fids:
             if a != b and b.startswith(a + "-"):
@@ -195,6 +200,22 @@ def _profile_memo(profile, memo: dict | None) -> dict:
     return hit[1]
 
 
+def _counts_array(trace) -> np.ndarray:
+    """int32 counts of a trace (this package's traces cache the array; the
+    reference's WorkloadTrace only has the tuple)."""
+    arr = getattr(trace, "array", None)
+    return arr() if arr is not None else np.array(trace.counts, np.int32)
+
+
+def _point_table(profile, memo: dict | None) -> dict:
+    """{(sm, quota): ProfileEntry} of a profile (per-call memo)."""
+    m = _profile_memo(profile, memo)
+    tab = m.get("table")
+    if tab is None:
+        tab = m["table"] = {(p.sm_partition, p.quota): e for p, e in profile.entries.items()}
+    return tab
+
+
 def _t_eff(lo: "_LoweredProfile") -> float:
     """Throughput of most_efficient_point (autoscaler.py:98-100)."""
     return float(lo.rows["thr"][lo.p_eff])
@@ -210,8 +231,8 @@ def _default_caps(scenario, fns, lowered) -> Caps:
     per_fn = 0
     for fn, lo in zip(fns, lowered):
         t_eff = _t_eff(lo)
-        counts = fn.trace.counts[:scenario.windows]
-        peak = max(counts, default=0) / window_s
+        counts = _counts_array(fn.trace)[:scenario.windows]
+        peak = (int(counts.max()) if len(counts) else 0) / window_s
         # t_eff <= 0: the first scale-up raises (autoscaler.py:115-117), so
         # the function never adds pods beyond its initial ones
         grow = int(math.ceil(1.5 * peak / t_eff)) if t_eff > 0 else 0
@@ -300,14 +321,38 @@ class RunImage:
     policy: str
     fids: list
     scen: np.ndarray
-    funcs: np.ndarray
-    points: np.ndarray
+    funcs: np.ndarray           # point_off: offset into ``points`` (this run)
+    point_blocks: list          # per function, read-only, shared between runs
     inits: np.ndarray
     counts: np.ndarray
     names: bytes
     scale_x: int
     scale_y: int
     point_keys: list          # per function: [(sm, quota)] in point order
+
+    @property
+    def points(self) -> np.ndarray:
+        """This run's point table (the functions' blocks, concatenated)."""
+        if not self.point_blocks:
+            return np.zeros(0, POINT_DT)
+        return np.concatenate(self.point_blocks)
+
+
+def _point_block(lo: "_LoweredProfile", lx: int, ly: int, memo: dict | None) -> np.ndarray:
+    """Device point rows of one lowered profile on a run's (lx, ly) grid.  The
+    block is read-only and shared by every function / run of the call with
+    the same profile and grid, so a batch uploads it once."""
+    key = ("block", id(lo), lx, ly)
+    hit = memo.get(key) if memo is not None else None
+    if hit is not None and hit[0] is lo:
+        return hit[1]
+    block = lo.rows.copy()
+    block["rect_w"] = [n * (lx // d) for n, d in zip(lo.w_num, lo.w_den)]
+    block["rect_h"] = [n * (ly // d) for n, d in zip(lo.h_num, lo.h_den)]
+    block.flags.writeable = False
+    if memo is not None:
+        memo[key] = (lo, block)
+    return block
 
 
 def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
@@ -316,13 +361,11 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
     ONE batch compile (per-profile-object cache; never reuse it across calls)."""
     if policy not in POLICIES:
         raise ValidationError(f"policy must be one of {POLICIES}, got {policy!r}")
-    validate_scenario(scenario)
+    validate_scenario(scenario, memo)
     fns = _ordered_functions(scenario)
     fids = [fn.function_id for fn in fns]
     timeshare = policy == "timeshare"
-    tables = []
-    for fn in fns:
-        tables.append({(p.sm_partition, p.quota): e for p, e in fn.profile.entries.items()})
+    tables = [_point_table(fn.profile, memo) for fn in fns]
     if timeshare:
         for fid, tab in zip(fids, tables):
             if (100.0, 1.0) not in tab:
@@ -358,71 +401,136 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
 
     windows = int(scenario.windows)
     n_f = len(fns)
-    funcs = np.zeros(n_f, FUNCTION_DT)
-    point_blocks, init_rows, point_keys = [], [], []
+    point_blocks, init_rows, point_keys, frows, traces = [], [], [], [], []
     n_points = 0
-    counts = np.zeros(n_f * windows, np.int32)
-    names = b""
+    names = []
+    name_off = 0
     sm_integral = all(lo.sm_integral for lo in lowered)
     for fi, (fn, lo) in enumerate(zip(fns, lowered)):
-        block = lo.rows.copy()
-        block["rect_w"] = [n * (lx // d) for n, d in zip(lo.w_num, lo.w_den)]
-        block["rect_h"] = [n * (ly // d) for n, d in zip(lo.h_num, lo.h_den)]
-        point_blocks.append(block)
+        point_blocks.append(_point_block(lo, lx, ly, memo))
         point_keys.append(lo.keys)
+        n_init = len(fn.initial_pods)
         for init in fn.initial_pods:
             k = (init.point.sm_partition, init.point.quota)
             has = init.quota_request is not None
             init_rows.append((lo.index[k], 1 if has else 0,
                               float(init.quota_request) if has else 0.0))
-        trace = list(fn.trace.counts[:windows])
-        counts[fi * windows: fi * windows + len(trace)] = trace
+        tc = _counts_array(fn.trace)
+        traces.append(tc if len(tc) <= windows else tc[:windows])
         raw = fn.function_id.encode("utf-8")
-        f = funcs[fi]
-        f["n_points"] = len(lo.keys)
-        f["point_off"] = n_points
-        n_points += len(lo.keys)
-        f["n_init"] = len(fn.initial_pods)
-        f["init_off"] = len(init_rows) - len(fn.initial_pods)
-        f["count_off"] = fi * windows
+        mem = fn.profile.mem
         # None = unbounded (-1 on the device).  A negative limit makes the
         # reference's `len(fn.queue) >= limit` (sim_engine.py:476) always true,
         # exactly like 0: every arrival is dropped.
-        f["max_queue"] = -1 if fn.max_queue is None else max(0, int(fn.max_queue))
-        f["p_eff"] = lo.p_eff
-        f["id_rank"] = rank[fn.function_id]
-        f["name_off"] = len(names)
-        f["name_len"] = len(raw)
-        f["slo_ms"] = fn.profile.slo_latency_ms
-        mem = fn.profile.mem
-        f["mem_server_mb"] = mem.mem_server_mb
-        f["mem_runtime_mb"] = mem.mem_runtime_mb
-        f["mem_noshare_mb"] = mem.mem_noshare_mb
-        names += raw
+        mq = -1 if fn.max_queue is None else max(0, int(fn.max_queue))
+        frows.append((len(lo.keys), n_points, n_init, len(init_rows) - n_init, fi * windows,
+                      mq, lo.p_eff, rank[fn.function_id], name_off, len(raw),
+                      fn.profile.slo_latency_ms, mem.mem_server_mb, mem.mem_runtime_mb,
+                      mem.mem_noshare_mb))
+        n_points += len(lo.keys)
+        name_off += len(raw)
+        names.append(raw)
+    funcs = np.array(frows, FUNCTION_DT) if frows else np.zeros(0, FUNCTION_DT)
+    if all(len(t) == windows for t in traces):
+        counts = np.concatenate(traces) if traces else np.zeros(0, np.int32)
+    else:
+        counts = np.zeros(n_f * windows, np.int32)
+        for fi, t in enumerate(traces):
+            counts[fi * windows: fi * windows + len(t)] = t
+    names = b"".join(names)
 
-    scen = np.zeros(1, SCENARIO_DT)
-    s = scen[0]
     window_s = scenario.window_ms / 1000.0
-    s["n_nodes"] = n_nodes
-    s["n_funcs"] = n_f
-    s["windows"] = windows
-    s["steps"] = steps_per_window(scenario.quantum)
-    s["epoch_windows"] = scenario.epoch_windows
-    s["cold_start_windows"] = scenario.cold_start_windows
-    s["restructure_threshold"] = scenario.restructure_threshold
-    s["flags"] = ((GS_FLAG_TIMESHARE if timeshare else 0)
-                  | (GS_FLAG_SHARING if scenario.model_sharing else 0)
-                  | (GS_FLAG_SM_INTEGRAL if sm_integral else 0))
-    s["side_x"], s["side_y"] = side_x, side_y
-    s["cap_pods"], s["cap_rects"], s["cap_returned"] = caps.pods, caps.rects, caps.returned
-    s["hot_class"] = caps.hot_class
-    s["window_s"] = window_s
-    s["quantum_s"] = window_s * scenario.quantum
-    s["quantum"] = scenario.quantum
-    s["capacity_mb"] = scenario.gpu_capacity_mb
-    points = np.concatenate(point_blocks) if point_blocks else np.zeros(0, POINT_DT)
-    return RunImage(policy, fids, scen, funcs, points,
+    scen = np.array([(
+        n_nodes, n_f, windows, steps_per_window(scenario.quantum), scenario.epoch_windows,
+        scenario.cold_start_windows, scenario.restructure_threshold,
+        ((GS_FLAG_TIMESHARE if timeshare else 0)
+         | (GS_FLAG_SHARING if scenario.model_sharing else 0)
+         | (GS_FLAG_SM_INTEGRAL if sm_integral else 0)),
+        0, side_x, side_y, caps.pods, caps.rects, caps.returned, caps.hot_class,
+        0, 0, 0, 0, window_s, window_s * scenario.quantum, scenario.quantum,
+        scenario.gpu_capacity_mb)], SCENARIO_DT)
+    return RunImage(policy, fids, scen, funcs, point_blocks,
                     np.array(init_rows, INIT_DT), counts, names, lx, ly, point_keys)
+
+
+_POOL_MIN_RUNS = 256          # below this a fork pool costs more than it saves
+
+
+def _compile_span(scenarios, policies, caps, lo, hi):
+    """compile_run over inputs [lo, hi) with one shared memo (== one call)."""
+    memo: dict = {}
+    out = []
+    for i in range(lo, hi):
+        try:
+            out.append(compile_run(scenarios[i], policies[i], caps, memo))
+        except Exception as exc:           # shipped back, raised in input order
+            out.append(exc)
+    return out
+
+
+_FORK_STATE = None
+
+
+def _forked_part(span):
+    """Worker body: compile a span and pack it into one Batch part; only the
+    packed arrays and the per-run metadata (no count arrays) travel back."""
+    sc, pol, caps = _FORK_STATE
+    res = _compile_span(sc, pol, caps, span[0], span[1])
+    ok = [k for k, r in enumerate(res) if isinstance(r, RunImage)]
+    part = Batch([res[k] for k in ok]) if ok else None
+    for k in ok:
+        res[k].counts = None              # the part holds them
+    return part, res
+
+
+def compile_batch(scenarios, policies, caps: Caps | None = None, *,
+                  workers: int | None = None):
+    """Lower a batch of (scenario, policy) runs on all host cores.
+
+    Returns ``(batch, index, errors)``: ``batch`` holds the runs that compiled,
+    in input order, ``index[j]`` is the input position of batch run ``j`` and
+    ``errors`` maps the other input positions to the exception
+    ``compile_run`` raised for them.  Large batches are lowered by a fork pool:
+    the scenario objects reach the workers copy-on-write, each worker packs
+    its span into a ``Batch`` part, and the parts are concatenated here.
+    Profile-derived data is shared by the runs of one span only (see
+    ``_profile_memo``)."""
+    import os
+    global _FORK_STATE
+    if not (hasattr(scenarios, "__getitem__") and hasattr(scenarios, "__len__")):
+        scenarios = list(scenarios)       # a lazy sequence stays lazy (built in the workers)
+    policies = list(policies)
+    n = len(scenarios)
+    workers = workers if workers is not None else (os.cpu_count() or 1)
+    if n < _POOL_MIN_RUNS or workers <= 1:
+        res = _compile_span(scenarios, policies, caps, 0, n)
+        index = [i for i, r in enumerate(res) if isinstance(r, RunImage)]
+        errors = {i: r for i, r in enumerate(res) if not isinstance(r, RunImage)}
+        return Batch([res[i] for i in index]), index, errors
+    import multiprocessing as mp
+    chunks = workers * 2
+    bounds = [(n * k // chunks, n * (k + 1) // chunks) for k in range(chunks)]
+    _FORK_STATE = (scenarios, policies, caps)
+    # freeze the heap before forking: a child's collector would otherwise walk
+    # (and so copy-on-write fault) every object of the parent
+    import gc
+    gc.freeze()
+    try:
+        with mp.get_context("fork").Pool(workers) as pool:
+            got = pool.map(_forked_part, bounds, chunksize=1)
+    finally:
+        _FORK_STATE = None
+        gc.unfreeze()
+    index, errors, parts = [], {}, []
+    for (lo, _hi), (part, res) in zip(bounds, got):
+        for k, r in enumerate(res):
+            if isinstance(r, RunImage):
+                index.append(lo + k)
+            else:
+                errors[lo + k] = r
+        if part is not None:
+            parts.append(part)
+    return Batch.concat(parts), index, errors
 
 
 class Batch:
@@ -435,7 +543,14 @@ class Batch:
         f_off = p_off = i_off = c_off = n_off = 0
         fn_rows = gpu_rows = glob_rows = places = 0
         funcs, points, inits, counts, names = [], [], [], [], []
+        # point blocks are deduplicated: by object, then by content
+        seen: dict = {}
+        by_content: dict = {}
+        keep: list = []           # holds the blocks so ids in `seen` stay unique
         for r, im in enumerate(images):
+            if im.counts is None:
+                raise ValueError("this RunImage was packed by compile_batch; "
+                                 "use Batch.prefix() / the batch it came with")
             s = im.scen.copy()
             s["func_off"] = f_off
             s["fn_row_off"] = fn_rows
@@ -449,17 +564,26 @@ class Batch:
             places += int(s["cap_pods"][0])
             self.runs[r] = s[0]
             fc = im.funcs.copy()
-            fc["point_off"] += p_off
+            for fi, block in enumerate(im.point_blocks):
+                off = seen.get(id(block))
+                if off is None:
+                    ck = block.tobytes()
+                    off = by_content.get(ck)
+                    if off is None:
+                        off = by_content[ck] = p_off
+                        points.append(block)
+                        p_off += len(block)
+                    seen[id(block)] = off
+                    keep.append(block)
+                fc["point_off"][fi] = off
             fc["init_off"] += i_off
             fc["count_off"] += c_off
             fc["name_off"] += n_off
             funcs.append(fc)
-            points.append(im.points)
             inits.append(im.inits)
             counts.append(im.counts)
             names.append(im.names)
             f_off += len(fc)
-            p_off += len(im.points)
             i_off += len(im.inits)
             c_off += len(im.counts)
             n_off += len(im.names)
@@ -478,6 +602,83 @@ class Batch:
 
     def __len__(self):
         return len(self.images)
+
+    @classmethod
+    def concat(cls, parts: list) -> "Batch":
+        """One batch from consecutive parts (offsets rebased, arrays joined)."""
+        b = cls([])
+        if not parts:
+            return b
+        runs, funcs, points = [], [], []
+        by_content: dict = {}                     # point blocks, deduplicated across parts
+        f_off = p_off = i_off = c_off = n_off = 0
+        fn_rows = gpu_rows = glob_rows = places = 0
+        for part in parts:
+            r = part.runs.copy()
+            r["func_off"] += f_off
+            r["fn_row_off"] += fn_rows
+            r["gpu_row_off"] += gpu_rows
+            r["glob_row_off"] += glob_rows
+            r["place_off"] += places
+            fc = part.funcs.copy()
+            starts, first, inv = np.unique(fc["point_off"], return_index=True,
+                                           return_inverse=True)
+            remap = np.empty(len(starts), np.int64)
+            for u, (st, k) in enumerate(zip(starts.tolist(), first.tolist())):
+                block = part.points[st: st + int(fc["n_points"][k])]
+                key = block.tobytes()
+                off = by_content.get(key)
+                if off is None:
+                    off = by_content[key] = p_off
+                    points.append(block)
+                    p_off += len(block)
+                remap[u] = off
+            fc["point_off"] = remap[inv.reshape(-1)]
+            fc["init_off"] += i_off
+            fc["count_off"] += c_off
+            fc["name_off"] += n_off
+            runs.append(r)
+            funcs.append(fc)
+            f_off += len(fc)
+            i_off += part.n_inits
+            c_off += len(part.counts)
+            n_off += len(part.names) - 1          # each part ends with one NUL
+            fn_rows += part.n_fn_rows
+            gpu_rows += part.n_gpu_rows
+            glob_rows += part.n_glob_rows
+            places += part.n_placements
+        b.images = [im for part in parts for im in part.images]
+        b.runs = np.concatenate(runs)
+        b.funcs = np.concatenate(funcs)
+        b.points = np.concatenate(points) if points else np.zeros(0, POINT_DT)
+        b.inits = np.concatenate([p.inits[:p.n_inits] for p in parts] + [np.zeros(1, INIT_DT)])
+        b.counts = np.ascontiguousarray(np.concatenate([p.counts for p in parts]), np.int32)
+        b.names = np.concatenate([p.names[:-1] for p in parts] + [np.zeros(1, np.uint8)])
+        b.n_fn_rows, b.n_gpu_rows, b.n_glob_rows = fn_rows, gpu_rows, glob_rows
+        b.n_placements = places
+        b.n_inits = i_off
+        return b
+
+    def prefix(self, n: int) -> "Batch":
+        """The first ``n`` runs as a batch with the identical layout (row and
+        placement offsets unchanged), e.g. a CPU-sample of a device batch."""
+        b = Batch([])
+        b.images = self.images[:n]
+        b.runs = self.runs[:n].copy()
+        nf = int(self.runs["func_off"][n]) if n < len(self) else len(self.funcs)
+        b.funcs = self.funcs[:nf].copy()
+        b.points, b.inits, b.counts, b.names = self.points, self.inits, self.counts, self.names
+        b.n_inits = self.n_inits
+        last = self.runs[n - 1] if n else None
+        if last is None:
+            b.n_fn_rows = b.n_gpu_rows = b.n_glob_rows = b.n_placements = 0
+        else:
+            W = int(last["windows"])
+            b.n_fn_rows = int(last["fn_row_off"]) + W * int(last["n_funcs"])
+            b.n_gpu_rows = int(last["gpu_row_off"]) + W * int(last["n_nodes"])
+            b.n_glob_rows = int(last["glob_row_off"]) + W
+            b.n_placements = int(last["place_off"]) + int(last["cap_pods"])
+        return b
 
     def alloc_outputs(self, rows: bool = True, pinned: bool = False):
         """Output arrays.  ``pinned=True`` places the row arrays in page-locked,

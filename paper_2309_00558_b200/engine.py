@@ -68,27 +68,11 @@ def run_error(image: cc.RunImage, status) -> Exception | None:
 
 def decode_run(batch: cc.Batch, r: int, out: dict) -> RunResult:
     """Rebuild the reference's report rows for run ``r`` from device records."""
+    from .report import decode_rows
     im = batch.images[r]
     s = batch.runs[r]
-    W, F, G = int(s["windows"]), int(s["n_funcs"]), int(s["n_nodes"])
-    rep = MetricsReport(policy=im.policy)
-    fn = out["fn_rows"][int(s["fn_row_off"]): int(s["fn_row_off"]) + W * F]
-    gp = out["gpu_rows"][int(s["gpu_row_off"]): int(s["gpu_row_off"]) + W * G]
-    gl = out["glob_rows"][int(s["glob_row_off"]): int(s["glob_row_off"]) + W]
-    fids = im.fids
-    fn_l = fn.tolist()
-    gp_l = gp.tolist()
-    gl_l = gl.tolist()
-    for w in range(W):
-        for f in range(F):
-            a, c, v, d, q = fn_l[w * F + f]
-            rep.function_rows.append(FunctionWindowRow(w, fids[f], a, c, v, d, q))
-        for g in range(G):
-            u, o, m, present, _ = gp_l[w * G + g]
-            if present:
-                rep.gpu_rows.append(GpuWindowRow(w, g, u, o, m))
-        n_use, fails, frag = gl_l[w]
-        rep.global_rows.append(GlobalWindowRow(w, n_use, fails, frag))
+    G = int(s["n_nodes"])
+    rep = MetricsReport(im.policy, *decode_rows(batch, out, r))
     st = out["status"][r]
     res = RunResult(rep, token_grants=int(st["token_grants"]),
                     scale_decisions=int(st["scale_decisions"]),
@@ -97,6 +81,7 @@ def decode_run(batch: cc.Batch, r: int, out: dict) -> RunResult:
                     pod_steps=int(st["pod_steps"]), rect_scans=int(st["rect_scans"]),
                     peak_pods=int(st["peak_pods"]))
     pl = out["placements"][int(s["place_off"]): int(s["place_off"]) + int(st["n_placements"])]
+    fids = im.fids
     nodes: dict = {g: {} for g in range(G)}
     for node, func, counter, x, y, w_, h, _ in pl.tolist():
         pod_id = f"{fids[func]}-{counter:04d}"
@@ -130,18 +115,16 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
     scenarios, policies = _normalise(scenarios, policies)
     results: list = [None] * len(scenarios)
     images: list = [None] * len(scenarios)
-    for i, (sc, pol) in enumerate(zip(scenarios, policies)):
-        try:
-            images[i] = cc.compile_run(sc, pol, caps)
-        except ValidationError as exc:
-            if errors == "raise":
-                raise
-            results[i] = exc
-    pending = [i for i in range(len(scenarios)) if images[i] is not None]
+    batch, pending, failed = cc.compile_batch(scenarios, policies, caps)
+    for i, exc in sorted(failed.items()):
+        if errors == "raise" or not isinstance(exc, ValidationError):
+            raise exc
+        results[i] = exc
     for _attempt in range(_MAX_CAP_RETRIES):
         if not pending:
             break
-        batch = cc.Batch([images[i] for i in pending])
+        if batch is None:
+            batch = cc.Batch([images[i] for i in pending])
         out = backend.run_batch(batch, device=device, rows=True)
         retry = []
         for j, i in enumerate(pending):
@@ -162,6 +145,7 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
             else:
                 results[i] = (batch, out, j)
         pending = retry
+        batch = None
     for i in pending:
         err = CapacityError("run still exceeds device capacities after "
                             f"{_MAX_CAP_RETRIES} enlargements")
@@ -184,14 +168,30 @@ def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "rais
 
 
 def run_batch(scenarios, policies="fast", *, device: int = 0, errors: str = "raise") -> list:
-    """Batch form of ``run``: one ``MetricsReport`` (or exception) per input."""
-    return [r.report if isinstance(r, RunResult) else r
-            for r in simulate(scenarios, policies, device=device, errors=errors)]
+    """Batch form of ``run``: one ``MetricsReport`` (or exception) per input.
+
+    The reports are ``report.DeviceReport``s: rows stay in the device records
+    until touched, ``to_csv()`` renders natively and ``summary()`` comes from
+    one vectorised reduction over the whole batch -- same values, same bytes."""
+    from .report import DeviceReport, SharedOutputs
+    recs = simulate_records(scenarios, policies, device=device, errors=errors)
+    shared: dict = {}
+    reps = []
+    for r in recs:
+        if isinstance(r, Exception):
+            reps.append(r)
+            continue
+        batch, out, j = r
+        sh = shared.get(id(out))
+        if sh is None:
+            sh = shared[id(out)] = SharedOutputs(batch, out)
+        reps.append(DeviceReport(sh, j))
+    return reps
 
 
 def run(scenario, policy: str = "fast") -> MetricsReport:
     """Simulate one scenario under one policy (sim_engine.py:601-603)."""
-    return simulate([scenario], [policy])[0].report
+    return run_batch([scenario], [policy])[0]
 
 
 def compare_policies(scenario, policies=POLICIES) -> dict:
@@ -199,5 +199,5 @@ def compare_policies(scenario, policies=POLICIES) -> dict:
     for p in policies:
         if p not in POLICIES:
             raise ValidationError(f"unknown policy {p!r}")
-    res = simulate([scenario] * len(policies), list(policies))
-    return {p: r.report for p, r in zip(policies, res)}
+    res = run_batch([scenario] * len(policies), list(policies))
+    return dict(zip(policies, res))

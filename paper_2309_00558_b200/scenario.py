@@ -125,10 +125,12 @@ def steps_per_window(quantum: float) -> int:
     return round(1.0 / quantum)
 
 
-def validate_scenario(sc) -> None:
+def validate_scenario(sc, memo: dict | None = None) -> None:
     """Scenario preconditions, in the reference's order (sim_engine.py:132-170).
 
     Works on this package's ``Scenario`` and on the reference's (duck typed).
+    ``memo``: the compiler's per-call dict; a profile object whose full-quota
+    points were checked earlier in the same call is not re-checked.
     """
     def need(ok, msg):
         if not ok:
@@ -153,10 +155,14 @@ def validate_scenario(sc) -> None:
         need(fid not in seen, f"duplicate function id {fid!r}")
         seen.add(fid)
         entries = fn.profile.entries
-        for sm in sorted({p.sm_partition for p in entries}):
-            need(_point(sm, 1.0, fn) in entries,
-                 f"{fid}: profile needs the full-quota point ({sm:g}, 1.0) "
-                 f"to derive the serving rate")
+        done = memo is not None and memo.get(("full-quota", id(fn.profile))) is fn.profile
+        if not done:
+            for sm in sorted({p.sm_partition for p in entries}):
+                need(_point(sm, 1.0, fn) in entries,
+                     f"{fid}: profile needs the full-quota point ({sm:g}, 1.0) "
+                     f"to derive the serving rate")
+            if memo is not None:
+                memo[("full-quota", id(fn.profile))] = fn.profile
         for init in fn.initial_pods:
             need(init.point in entries,
                  f"{fid}: initial pod point ({init.point.sm_partition:g}, "

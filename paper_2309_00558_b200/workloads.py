@@ -158,3 +158,25 @@ def c2_scenarios(seeds, windows: int = 300):
         out.append(Scenario(fleet_size=4, windows=windows, functions=fns, epoch_windows=5,
                             quantum=0.02, cold_start_windows=2, seed=seed, model_sharing=True))
     return out
+
+
+class ScenarioSeq:
+    """A sequence of ``n`` scenarios built on first access by ``make(i)`` (a
+    Scenario, or a scenario dict).  ``compiler.compile_batch`` indexes it
+    inside its worker processes, so large sweeps are also *generated* on all
+    host cores."""
+
+    def __init__(self, make, n: int):
+        self.make, self.n = make, n
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __getitem__(self, i: int):
+        if not 0 <= i < self.n:
+            raise IndexError(i)
+        x = self.make(i)
+        if isinstance(x, dict):
+            from .scenario import Scenario
+            x = Scenario.from_dict(x)
+        return x

@@ -1,0 +1,129 @@
+"""Host fast path, CPU only: the parallel batch compiler,
+the native CSV / number renderer (csrc/gs_host.cpp, called through the C
+ABI without a GPU) and the lazy DeviceReport, each against the plain Python
+path it replaces.  Device outputs are produced by the oracle here."""
+import pickle
+import random
+import struct
+
+import numpy as np
+import pytest
+
+import golden
+import oracle
+from paper_2309_00558_b200 import compiler as cc, engine, report, workloads as wl
+from paper_2309_00558_b200.errors import ValidationError
+from paper_2309_00558_b200.metrics import MetricsReport
+from paper_2309_00558_b200.scenario import Scenario
+from paper_2309_00558_b200.util import fmt_num
+
+
+def _values():
+    rng = random.Random(7)
+    v = [rng.random() for _ in range(4000)]
+    v += [rng.random() * 10 ** rng.randint(-25, 25) for _ in range(4000)]
+    v += [struct.unpack("d", struct.pack("Q", rng.getrandbits(64)))[0] for _ in range(4000)]
+    v += [2.0 ** k for k in range(-1074, 1024, 3)] + [-(2.0 ** k) for k in range(-60, 60)]
+    v += [k / 1e9 + 5e-10 for k in range(2000)] + [k / 1e6 + 5e-7 for k in range(2000)]
+    v += [0.0, -0.0, 1e15, 1e16, 999999999999999.9, 1e-4, 1e-5, 0.5, 2.5, 1.0 / 3,
+          float("inf"), -float("inf"), float("nan"), 5e-324, 1.7976931348623157e308]
+    return v
+
+
+@pytest.mark.parametrize("nd", [9, 6, -1])
+def test_native_numbers_match_the_interpreter(nd):
+    vals = _values()
+    got = report.format_numbers(vals, nd)
+    want = [fmt_num(round(x, nd) if nd >= 0 else x) for x in vals]
+    bad = [(x, g, w) for x, g, w in zip(vals, got, want) if g != w]
+    assert not bad, bad[:5]
+
+
+def _oracle_batch(scen, pols):
+    batch, index, errors = cc.compile_batch(scen, pols)
+    assert not errors
+    return batch, oracle.run_batch(batch, n_threads=4)
+
+
+def test_native_csv_matches_metrics_report_on_goldens():
+    recs = [r for r in golden.records() if "error" not in r["expect"]][:200]
+    scen = [golden.load_scenario(r) for r in recs]
+    batch, out = _oracle_batch(scen, [r["policy"] for r in recs])
+    texts = report.csv_texts(batch, out)
+    sums = report.summaries(batch, out)
+    for j, rec in enumerate(recs):
+        assert texts[j] == rec["expect"]["csv"], rec["name"]
+        assert sums[j] == rec["expect"]["summary"], rec["name"]
+
+
+def test_native_csv_quotes_function_ids_like_csv_writer():
+    d = wl.c2(3, windows=12, n_funcs=3, fleet=2)
+    for fn, fid in zip(d["functions"], ['a,b', 'q"x', 'café']):
+        fn["function_id"] = fid
+    sc = Scenario.from_dict(d)
+    batch, out = _oracle_batch([sc, sc], ["fast", "timeshare"])
+    for j in range(2):
+        want = engine.decode_run(batch, j, out).report
+        assert report.csv_texts(batch, out, range(j, j + 1))[0] == want.to_csv()
+
+
+def test_device_report_is_a_lazy_metrics_report():
+    scen = [Scenario.from_dict(wl.c3(s, windows=30)) for s in range(6)]
+    pols = ["fast", "timeshare"] * 3
+    batch, out = _oracle_batch(scen, pols)
+    sh = report.SharedOutputs(batch, out)
+    for j in range(len(batch)):
+        want = engine.decode_run(batch, j, out).report
+        lazy = report.DeviceReport(sh, j)
+        assert isinstance(lazy, MetricsReport) and lazy._rows is None
+        assert lazy.to_csv() == want.to_csv()
+        s1 = lazy.summary()
+        s1["policy"] = "mutated"                       # callers own the dict
+        assert lazy.summary() == want.summary()
+        assert lazy._rows is None                      # nothing materialised so far
+        assert lazy == want and want == lazy
+        assert lazy.function_rows == want.function_rows
+        plain = pickle.loads(pickle.dumps(lazy))
+        assert type(plain) is MetricsReport and plain == want
+        # editing materialised rows is honoured by the inherited renderers
+        lazy.function_rows.pop()
+        assert lazy.to_csv() == MetricsReport(lazy.policy, lazy.function_rows,
+                                              lazy.gpu_rows, lazy.global_rows).to_csv()
+        assert lazy != want
+
+
+def test_compile_batch_pool_matches_serial_compile():
+    seq = wl.ScenarioSeq(lambda i: wl.c5(i * 37), 600)
+    pols = ["fast"] * 600
+    pooled, idx, err = cc.compile_batch(seq, pols, workers=4)
+    serial = cc.Batch([cc.compile_run(seq[i], "fast") for i in range(600)])
+    assert idx == list(range(600)) and not err
+    for name in cc.SCENARIO_DT.names:
+        assert np.array_equal(pooled.runs[name], serial.runs[name]), name
+    assert np.array_equal(pooled.counts, serial.counts)
+    for f in range(len(serial.funcs)):                 # point blocks are deduplicated
+        a, b = pooled.funcs[f], serial.funcs[f]
+        n = int(b["n_points"])
+        assert pooled.points[a["point_off"]: a["point_off"] + n].tobytes() == \
+            serial.points[b["point_off"]: b["point_off"] + n].tobytes()
+    assert len(pooled.points) == len(serial.points)       # deduplicated across parts too
+    assert pooled.names.tobytes() == serial.names.tobytes()
+    o1 = oracle.run_batch(pooled.prefix(60), n_threads=4)
+    o2 = oracle.run_batch(serial.prefix(60), n_threads=4)
+    for k in ("fn_rows", "gpu_rows", "glob_rows", "summary"):
+        n = len(o2[k]) if k == "summary" else None
+        assert o1[k][:n].tobytes() == o2[k][:n].tobytes(), k
+
+
+def test_compile_batch_reports_errors_in_input_order():
+    good = Scenario.from_dict(wl.c1())
+    bad = Scenario.from_dict(wl.c1())
+    bad.functions[0].initial_pods.append(type(bad.functions[0].initial_pods[0])(
+        type(bad.functions[0].initial_pods[0].point)(13.0, 0.4), None))
+    seq = [good] * 300 + [bad] + [good] * 50
+    batch, idx, err = cc.compile_batch(seq, ["fast"] * len(seq), workers=3)
+    assert list(err) == [300] and isinstance(err[300], ValidationError)
+    assert "is not profiled" in str(err[300])
+    assert len(batch) == 350 and idx == list(range(300)) + list(range(301, 351))
+    with pytest.raises(ValueError):
+        cc.Batch([batch.images[0]])                    # packed images carry no counts

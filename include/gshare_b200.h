@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 enum {
   GS_OK = 0,
@@ -103,6 +103,8 @@ typedef struct gs_function {
   int32_t p_eff;                 /* most_efficient_point index (autoscaler.py:98)*/
   int32_t id_rank;               /* rank of fid+"-" : pod-id string order        */
   int32_t name_off, name_len;    /* UTF-8 function id in gs_batch_t.names        */
+  int32_t n_id_splits;           /* pod-id order segments beyond the first       */
+  int32_t id_split_off;          /* first gs_id_split_t of this function         */
   double slo_ms;
   double mem_server_mb, mem_runtime_mb, mem_noshare_mb;
 } gs_function_t;
@@ -119,6 +121,20 @@ typedef struct gs_point {
   int32_t rate_ok, pad;          /* T(sm_eff,1.0) > 0                            */
 } gs_point_t;
 
+/* Pod-id string order (pod ids are f"{fid}-{counter:04d}", sim_engine.py:354;
+ * many tie-breaks compare them as strings).  A pod's 64-bit order key is
+ * slot * 11^10 + digits_key(counter), digits_key = the counter's decimal text
+ * in base 11 (0 = end of text), so keys compare exactly as the strings do.
+ * slot = id_rank unless the function id is extended by other ids with "-"
+ * (e.g. "x" and "x-1"): then the pods of "x" interleave with the pods of the
+ * extending ids at thresholds of the counter text, and slot = the slot of the
+ * last split whose threshold is below digits_key(counter). */
+typedef struct gs_id_split {
+  uint64_t threshold;            /* digits_key space                             */
+  int32_t slot;
+  int32_t pad;
+} gs_id_split_t;
+
 typedef struct gs_init {
   int32_t point;                 /* index into the function's points             */
   int32_t has_q_req;             /* InitialPod.quota_request is not None         */
@@ -130,12 +146,14 @@ typedef struct gs_batch {
   int32_t n_funcs, n_points, n_inits;
   int64_t n_counts, n_names;
   int64_t n_fn_rows, n_gpu_rows, n_glob_rows, n_placements;
+  int64_t n_id_splits;
   const gs_scenario_t* runs;
   const gs_function_t* funcs;
   const gs_point_t* points;
   const gs_init_t* inits;
   const int32_t* counts;
   const char* names;
+  const gs_id_split_t* id_splits;  /* may be NULL when n_id_splits == 0          */
 } gs_batch_t;
 
 /* ---- outputs (metrics.py:27-52) ---------------------------------------- */

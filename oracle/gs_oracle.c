@@ -798,5 +798,6 @@ int gs_oracle_sizeof(const char* name) {
   if (!strcmp(name, "gs_summary_t")) return (int)sizeof(gs_summary_t);
   if (!strcmp(name, "gs_batch_t")) return (int)sizeof(gs_batch_t);
   if (!strcmp(name, "gs_out_t")) return (int)sizeof(gs_out_t);
+  if (!strcmp(name, "gs_id_split_t")) return (int)sizeof(gs_id_split_t);
   return -1;
 }

@@ -15,9 +15,10 @@ class GsBatch(C.Structure):
         ("n_runs", C.c_int32), ("n_funcs", C.c_int32), ("n_points", C.c_int32),
         ("n_inits", C.c_int32), ("n_counts", C.c_int64), ("n_names", C.c_int64),
         ("n_fn_rows", C.c_int64), ("n_gpu_rows", C.c_int64), ("n_glob_rows", C.c_int64),
-        ("n_placements", C.c_int64),
+        ("n_placements", C.c_int64), ("n_id_splits", C.c_int64),
         ("runs", C.c_void_p), ("funcs", C.c_void_p), ("points", C.c_void_p),
         ("inits", C.c_void_p), ("counts", C.c_void_p), ("names", C.c_void_p),
+        ("id_splits", C.c_void_p),
     ]
 
 
@@ -51,6 +52,8 @@ def make_batch_struct(batch) -> GsBatch:
     b.inits = _ptr(batch.inits)
     b.counts = _ptr(batch.counts)
     b.names = _ptr(batch.names)
+    b.n_id_splits = len(batch.id_splits)
+    b.id_splits = _ptr(batch.id_splits) if len(batch.id_splits) else None
     return b
 
 

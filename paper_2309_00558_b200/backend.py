@@ -73,7 +73,7 @@ def lib():
             L.gs_format_csv_batch.restype = i64
             L.gs_format_numbers.argtypes = [vp, i64, i, vp, i64]
             L.gs_format_numbers.restype = i
-            if L.gs_abi_version() != 1:
+            if L.gs_abi_version() != 2:
                 raise BackendUnavailableError("libgshare_b200.so ABI version mismatch")
             _lib = L
         return _lib

@@ -16,10 +16,11 @@ include/gshare_b200.h:
 * pod rectangles as integers: the packer's exact rationals
   (packer.py:39-53,129-133) are scaled by the lcm of their denominators so
   every coordinate, area and comparison is exact int64 arithmetic;
-* a pod-id order rank per function: pod ids are ``f"{fid}-{n:04d}"``
-  (sim_engine.py:354) and string order decides many tie-breaks; ranking
-  ``fid + "-"`` reproduces string order whenever no function id extends
-  another id followed by ``-`` (validated here).
+* a pod-id order per function: pod ids are ``f"{fid}-{n:04d}"``
+  (sim_engine.py:354) and string order decides many tie-breaks; each pod's
+  64-bit key is (slot, counter text), with the slots handed out over the
+  prefix forest of the ``fid + "-"`` strings so that ids extending other ids
+  ("x" and "x-1") interleave exactly as the strings do (``_pod_id_order``).
 """
 from __future__ import annotations
 
@@ -58,7 +59,7 @@ SCENARIO_DT = np.dtype([
 FUNCTION_DT = np.dtype([
     ("n_points", "<i4"), ("point_off", "<i4"), ("n_init", "<i4"), ("init_off", "<i4"),
     ("count_off", "<i4"), ("max_queue", "<i4"), ("p_eff", "<i4"), ("id_rank", "<i4"),
-    ("name_off", "<i4"), ("name_len", "<i4"),
+    ("name_off", "<i4"), ("name_len", "<i4"), ("n_id_splits", "<i4"), ("id_split_off", "<i4"),
     ("slo_ms", "<f8"), ("mem_server_mb", "<f8"), ("mem_runtime_mb", "<f8"),
     ("mem_noshare_mb", "<f8"),
 ], align=True)
@@ -68,6 +69,8 @@ POINT_DT = np.dtype([
     ("sm_eff", "<f8"), ("inv_rate", "<f8"), ("rect_w", "<i4"), ("rect_h", "<i4"),
     ("rate_ok", "<i4"), ("pad", "<i4"),
 ], align=True)
+
+ID_SPLIT_DT = np.dtype([("threshold", "<u8"), ("slot", "<i4"), ("pad", "<i4")], align=True)
 
 INIT_DT = np.dtype([("point", "<i4"), ("has_q_req", "<i4"), ("q_req", "<f8")], align=True)
 
@@ -100,6 +103,7 @@ STRUCT_SIZES = {  # checked against sizeof() of the C structs by the tests
     "gs_fn_row_t": FN_ROW_DT.itemsize, "gs_gpu_row_t": GPU_ROW_DT.itemsize,
     "gs_glob_row_t": GLOB_ROW_DT.itemsize, "gs_placement_t": PLACEMENT_DT.itemsize,
     "gs_status_t": STATUS_DT.itemsize, "gs_summary_t": SUMMARY_DT.itemsize,
+    "gs_id_split_t": ID_SPLIT_DT.itemsize,
 }
 
 # exactness limits of the device geometry
@@ -147,32 +151,82 @@ def _ordered_functions(scenario):
     return [fns[fid] for fid in sorted(fns)]
 
 
-def _check_pod_id_order(fids) -> dict:
-    """Rank of each fid such that pod-id string order == (rank, counter digits)."""
-    keyed = sorted(fids, key=lambda f: f + "-")
-    # keys sharing the prefix a+"-" sort contiguously right behind it, so a
-    # clash shows up between neighbours; only then search for the pair the
-    # reference-order double loop reports first
-    if all(not (b + "-").startswith(a + "-") for a, b in zip(keyed, keyed[1:])):
-        return {f: i for i, f in enumerate(keyed)}
-    for a in fids:
-        for b in fids:
-            if a != b and b.startswith(a + "-"):
-                raise ValidationError(
-                    f"function ids {a!r} and {b!r}: an id that extends another id "
-                    f"with '-' makes pod-id order counter dependent; not supported "
-                    f"by the CUDA backend")
-    return {f: i for i, f in enumerate(keyed)}
+def _digits_key_text(text: str) -> int:
+    """Order-preserving integer of a digit string of <= 10 characters: base 11,
+    digit d -> d + 1, 0 = end of text (so a prefix sorts first) -- the host
+    twin of the device's ``digits_key``."""
+    key = 0
+    for i in range(10):
+        key = key * 11 + ((ord(text[i]) - 47) if i < len(text) else 0)
+    return key
 
 
 def _digits_key(counter: int) -> int:
-    """Order-preserving integer for the text of f"{counter:04d}" (host twin of
-    the device's ``digits_key``)."""
-    s = "%04d" % counter
-    key = 0
-    for i in range(10):
-        key = key * 11 + ((ord(s[i]) - 47) if i < len(s) else 0)
-    return key
+    return _digits_key_text("%04d" % counter)
+
+
+def _split_threshold(rest: str) -> int:
+    """Pods "<fid>-<digits>" of a function vs the pods of an id that extends
+    it as "<fid>-<rest>": comparing <digits> with "<rest>-..." is decided
+    within the leading digit run d of "<rest>-" and the character c after
+    it (the digits can never reach the '-').  Returns T such that the pods
+    whose digits_key is <= T sort before the extending id's pods."""
+    t = rest + "-"
+    k = 0
+    while t[k] in "0123456789":
+        k += 1
+    d, c = t[:k], t[k]
+    if len(d) >= 10 or c < "0":
+        return _digits_key_text(d[:10])       # only counters <= d sort first
+    return _digits_key_text(d + "9" * (10 - len(d)))  # every counter starting with d too
+
+
+def _pod_id_order(fids):
+    """Pod-id string order as (first slot, [(threshold, slot)]) per function id.
+
+    Pod ids are f"{fid}-{n:04d}" (sim_engine.py:354).  Ids whose "fid-"
+    strings are not prefixes of one another order by that string alone: one
+    slot each, in sorted order.  When "a-" is a prefix of "b-" ("a" and
+    "a-1"), every pod of "b" lies in one contiguous block between pods of "a"
+    whose position depends only on the counter text of a's pod
+    (``_split_threshold``).  A depth-first walk of the prefix forest hands
+    out slots: a function's segments interleave with its extenders' blocks."""
+    keyed = sorted(fids, key=lambda f: f + "-")
+    children: dict = {f: [] for f in fids}
+    roots, stack = [], []
+    for g in keyed:
+        while stack and not (g + "-").startswith(stack[-1] + "-"):
+            stack.pop()
+        (children[stack[-1]] if stack else roots).append(g)
+        stack.append(g)
+    order: dict = {}
+    nxt = 0
+
+    def visit(f):
+        nonlocal nxt
+        first = nxt
+        nxt += 1
+        splits = []
+        for g in children[f]:
+            visit(g)
+            splits.append((_split_threshold(g[len(f) + 1:]), nxt))
+            nxt += 1
+        order[f] = (first, splits)
+
+    for r in roots:
+        visit(r)
+    return order
+
+
+def pod_order_key(order, fid: str, counter: int) -> int:
+    """The device's 64-bit pod order key (tests compare it with str order)."""
+    first, splits = order[fid]
+    dk = _digits_key(counter)
+    slot = first
+    for thr, s in splits:
+        if dk > thr:
+            slot = s
+    return slot * 11 ** 10 + dk
 
 
 def _resource_config_check(sm, q_req, q_lim):
@@ -329,6 +383,7 @@ class RunImage:
     scale_x: int
     scale_y: int
     point_keys: list          # per function: [(sm, quota)] in point order
+    id_splits: np.ndarray     # ID_SPLIT_DT, function-relative (id_split_off)
 
     @property
     def points(self) -> np.ndarray:
@@ -384,7 +439,7 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
                 raise ValidationError(
                     f"{fn.function_id}: zero serving rate at ({sm_eff:g}, 1.0)")
 
-    rank = _check_pod_id_order(fids)
+    order = _pod_id_order(fids)
     lowered = [_lower_profile(fn.profile, timeshare, memo) for fn in fns]
     caps = caps or _default_caps(scenario, fns, lowered)
 
@@ -401,7 +456,7 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
 
     windows = int(scenario.windows)
     n_f = len(fns)
-    point_blocks, init_rows, point_keys, frows, traces = [], [], [], [], []
+    point_blocks, init_rows, point_keys, frows, traces, id_splits = [], [], [], [], [], []
     n_points = 0
     names = []
     name_off = 0
@@ -423,13 +478,15 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
         # reference's `len(fn.queue) >= limit` (sim_engine.py:476) always true,
         # exactly like 0: every arrival is dropped.
         mq = -1 if fn.max_queue is None else max(0, int(fn.max_queue))
+        first, splits = order[fn.function_id]
         frows.append((len(lo.keys), n_points, n_init, len(init_rows) - n_init, fi * windows,
-                      mq, lo.p_eff, rank[fn.function_id], name_off, len(raw),
+                      mq, lo.p_eff, first, name_off, len(raw), len(splits), len(id_splits),
                       fn.profile.slo_latency_ms, mem.mem_server_mb, mem.mem_runtime_mb,
                       mem.mem_noshare_mb))
         n_points += len(lo.keys)
         name_off += len(raw)
         names.append(raw)
+        id_splits.extend((thr, slot, 0) for thr, slot in splits)
     funcs = np.array(frows, FUNCTION_DT) if frows else np.zeros(0, FUNCTION_DT)
     if all(len(t) == windows for t in traces):
         counts = np.concatenate(traces) if traces else np.zeros(0, np.int32)
@@ -450,7 +507,8 @@ def compile_run(scenario, policy: str = "fast", caps: Caps | None = None,
         0, 0, 0, 0, window_s, window_s * scenario.quantum, scenario.quantum,
         scenario.gpu_capacity_mb)], SCENARIO_DT)
     return RunImage(policy, fids, scen, funcs, point_blocks,
-                    np.array(init_rows, INIT_DT), counts, names, lx, ly, point_keys)
+                    np.array(init_rows, INIT_DT), counts, names, lx, ly, point_keys,
+                    np.array(id_splits, ID_SPLIT_DT))
 
 
 _POOL_MIN_RUNS = 256          # below this a fork pool costs more than it saves
@@ -542,7 +600,8 @@ class Batch:
         self.runs = np.zeros(n, SCENARIO_DT)
         f_off = p_off = i_off = c_off = n_off = 0
         fn_rows = gpu_rows = glob_rows = places = 0
-        funcs, points, inits, counts, names = [], [], [], [], []
+        funcs, points, inits, counts, names, splits = [], [], [], [], [], []
+        s_off = 0
         # point blocks are deduplicated: by object, then by content
         seen: dict = {}
         by_content: dict = {}
@@ -579,10 +638,13 @@ class Batch:
             fc["init_off"] += i_off
             fc["count_off"] += c_off
             fc["name_off"] += n_off
+            fc["id_split_off"] += s_off
             funcs.append(fc)
             inits.append(im.inits)
             counts.append(im.counts)
             names.append(im.names)
+            splits.append(im.id_splits)
+            s_off += len(im.id_splits)
             f_off += len(fc)
             i_off += len(im.inits)
             c_off += len(im.counts)
@@ -593,6 +655,7 @@ class Batch:
         self.counts = np.ascontiguousarray(np.concatenate(counts) if counts
                                            else np.zeros(0, np.int32), np.int32)
         self.names = np.frombuffer(b"".join(names) + b"\0", np.uint8).copy()
+        self.id_splits = np.concatenate(splits) if splits else np.zeros(0, ID_SPLIT_DT)
         self.n_fn_rows, self.n_gpu_rows = fn_rows, gpu_rows
         self.n_glob_rows, self.n_placements = glob_rows, places
         # keep at least one element so every pointer is valid
@@ -611,7 +674,7 @@ class Batch:
             return b
         runs, funcs, points = [], [], []
         by_content: dict = {}                     # point blocks, deduplicated across parts
-        f_off = p_off = i_off = c_off = n_off = 0
+        f_off = p_off = i_off = c_off = n_off = s_off = 0
         fn_rows = gpu_rows = glob_rows = places = 0
         for part in parts:
             r = part.runs.copy()
@@ -637,6 +700,8 @@ class Batch:
             fc["init_off"] += i_off
             fc["count_off"] += c_off
             fc["name_off"] += n_off
+            fc["id_split_off"] += s_off
+            s_off += len(part.id_splits)
             runs.append(r)
             funcs.append(fc)
             f_off += len(fc)
@@ -654,6 +719,7 @@ class Batch:
         b.inits = np.concatenate([p.inits[:p.n_inits] for p in parts] + [np.zeros(1, INIT_DT)])
         b.counts = np.ascontiguousarray(np.concatenate([p.counts for p in parts]), np.int32)
         b.names = np.concatenate([p.names[:-1] for p in parts] + [np.zeros(1, np.uint8)])
+        b.id_splits = np.concatenate([p.id_splits for p in parts])
         b.n_fn_rows, b.n_gpu_rows, b.n_glob_rows = fn_rows, gpu_rows, glob_rows
         b.n_placements = places
         b.n_inits = i_off
@@ -668,6 +734,7 @@ class Batch:
         nf = int(self.runs["func_off"][n]) if n < len(self) else len(self.funcs)
         b.funcs = self.funcs[:nf].copy()
         b.points, b.inits, b.counts, b.names = self.points, self.inits, self.counts, self.names
+        b.id_splits = self.id_splits
         b.n_inits = self.n_inits
         last = self.runs[n - 1] if n else None
         if last is None:
@@ -701,7 +768,7 @@ class Batch:
     def pin(self) -> "Batch":
         """Move the input arrays to page-locked host memory (fast H2D)."""
         from .backend import host_empty
-        for name in ("runs", "funcs", "points", "inits", "counts", "names"):
+        for name in ("runs", "funcs", "points", "inits", "counts", "names", "id_splits"):
             a = getattr(self, name)
             p = host_empty(len(a), a.dtype)
             p[:len(a)] = a
@@ -710,4 +777,4 @@ class Batch:
 
     def input_bytes(self) -> int:
         return sum(a.nbytes for a in (self.runs, self.funcs, self.points, self.inits,
-                                      self.counts, self.names))
+                                      self.counts, self.names, self.id_splits))

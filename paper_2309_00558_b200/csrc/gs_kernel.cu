@@ -533,6 +533,7 @@ gs_sim_kernel(KArgs a) {
     c.points = a.in.points;
     c.counts = a.in.counts;
     c.inits = a.in.inits;
+    c.splits = a.in.id_splits;
     c.G = c.sc->n_nodes; c.F = c.sc->n_funcs; c.P = c.sc->cap_pods; c.R = c.sc->cap_rects;
     c.RET = c.sc->cap_returned; c.W = c.sc->windows; c.T = c.sc->steps; c.flags = c.sc->flags;
     c.ws = c.sc->window_s; c.qs = c.sc->quantum_s; c.quantum = c.sc->quantum;
@@ -567,6 +568,7 @@ __global__ void __launch_bounds__(XL_THREADS, 1) gs_sim_kernel_xl(KArgs a) {
     c.points = a.in.points;
     c.counts = a.in.counts;
     c.inits = a.in.inits;
+    c.splits = a.in.id_splits;
     c.G = c.sc->n_nodes; c.F = c.sc->n_funcs; c.P = c.sc->cap_pods; c.R = c.sc->cap_rects;
     c.RET = c.sc->cap_returned; c.W = c.sc->windows; c.T = c.sc->steps; c.flags = c.sc->flags;
     c.ws = c.sc->window_s; c.qs = c.sc->quantum_s; c.quantum = c.sc->quantum;
@@ -714,6 +716,16 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
     cls[r] = run_class(sc);
     order[r] = r;
   }
+  for (int f = 0; f < in->n_funcs; f++) {
+    const gs_function_t& fn = in->funcs[f];
+    if (fn.n_id_splits < 0 || (fn.n_id_splits > 0 &&
+        (!in->id_splits || fn.id_split_off < 0 ||
+         (long long)fn.id_split_off + fn.n_id_splits > in->n_id_splits))) {
+      put_err(err, err_len, "malformed function record (pod-id order splits)");
+      delete s;
+      return GS_ERR_ARG;
+    }
+  }
   std::stable_sort(order.begin(), order.begin() + R, [&](int a, int b) {
     return cls[a] != cls[b] ? cls[a] < cls[b] : cost[a] > cost[b];
   });
@@ -732,6 +744,7 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   size_t o_inits = slot(nbytes<gs_init_t>(in->n_inits));
   size_t o_counts = slot(nbytes<int32_t>(in->n_counts));
   size_t o_names = slot(nbytes<char>(in->n_names));
+  size_t o_splits = slot(nbytes<gs_id_split_t>(in->n_id_splits));
   size_t in_end = off;
   size_t o_fn = slot(nbytes<gs_fn_row_t>(in->n_fn_rows));
   size_t o_gpu = slot(nbytes<gs_gpu_row_t>(in->n_gpu_rows));
@@ -764,6 +777,8 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   if (ce == cudaSuccess) ce = up(o_inits, in->inits, sizeof(gs_init_t) * (size_t)in->n_inits);
   if (ce == cudaSuccess) ce = up(o_counts, in->counts, sizeof(int32_t) * (size_t)in->n_counts);
   if (ce == cudaSuccess) ce = up(o_names, in->names, (size_t)in->n_names);
+  if (ce == cudaSuccess)
+    ce = up(o_splits, in->id_splits, sizeof(gs_id_split_t) * (size_t)in->n_id_splits);
   if (ce == cudaSuccess) ce = up(o_wsoff, ws_off.data(), sizeof(long long) * (size_t)R);
   if (ce == cudaSuccess) ce = up(o_order, order.data(), sizeof(int) * (size_t)R);
   if (ce != cudaSuccess) {
@@ -780,6 +795,7 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   s->dev_in.inits = reinterpret_cast<const gs_init_t*>(B + o_inits);
   s->dev_in.counts = reinterpret_cast<const int32_t*>(B + o_counts);
   s->dev_in.names = reinterpret_cast<const char*>(B + o_names);
+  s->dev_in.id_splits = reinterpret_cast<const gs_id_split_t*>(B + o_splits);
   s->dev_out.fn_rows = reinterpret_cast<gs_fn_row_t*>(B + o_fn);
   s->dev_out.gpu_rows = reinterpret_cast<gs_gpu_row_t*>(B + o_gpu);
   s->dev_out.glob_rows = reinterpret_cast<gs_glob_row_t*>(B + o_glob);
@@ -880,7 +896,8 @@ extern "C" int gs_session_upload(gs_session_t* s, const gs_batch_t* in, void* st
   if (in->n_runs != d.n_runs || in->n_funcs != d.n_funcs || in->n_points != d.n_points ||
       in->n_inits != d.n_inits || in->n_counts != d.n_counts || in->n_names != d.n_names ||
       in->n_fn_rows != d.n_fn_rows || in->n_gpu_rows != d.n_gpu_rows ||
-      in->n_glob_rows != d.n_glob_rows || in->n_placements != d.n_placements) {
+      in->n_glob_rows != d.n_glob_rows || in->n_placements != d.n_placements ||
+      in->n_id_splits != d.n_id_splits) {
     put_err(err, err_len, "gs_session_upload: batch shape differs from the session's");
     return GS_ERR_ARG;
   }
@@ -896,6 +913,7 @@ extern "C" int gs_session_upload(gs_session_t* s, const gs_batch_t* in, void* st
   CK(up(d.inits, in->inits, sizeof(gs_init_t) * (size_t)in->n_inits));
   CK(up(d.counts, in->counts, sizeof(int32_t) * (size_t)in->n_counts));
   CK(up(d.names, in->names, (size_t)in->n_names));
+  CK(up(d.id_splits, in->id_splits, sizeof(gs_id_split_t) * (size_t)in->n_id_splits));
   return GS_OK;
 }
 

@@ -70,19 +70,35 @@ __device__ __forceinline__ unsigned long long ord_key(double x) {
 
 // Order-preserving integer of the text f"{counter:04d}" (<= 10 digits):
 // base-11 digits with 0 as the "string ended" sentinel, so shorter strings
-// that are prefixes sort first -- exactly Python's str comparison.
+// that are prefixes sort first -- exactly Python's str comparison.  Digits
+// are taken least significant first; digit j (from the right) of an n-digit
+// text sits at base-11 position 10 - n + j.
 __device__ __forceinline__ unsigned long long digits_key(int counter) {
-  int d[10];
-  int n = 0;
   unsigned v = (unsigned)counter;
+  int n = 1;
   #pragma unroll 1
-  do { d[n++] = (int)(v % 10u); v /= 10u; } while (v && n < 10);
+  for (unsigned t = v / 10u; t && n < 10; t /= 10u) n++;
+  if (n < 4) n = 4;
+  unsigned long long w = 1, key = 0;
   #pragma unroll 1
-  while (n < 4) d[n++] = 0;
-  unsigned long long key = 0;
+  for (int i = n; i < 10; i++) w *= 11ull;
   #pragma unroll 1
-  for (int i = 0; i < 10; i++) key = key * 11ull + (i < n ? (unsigned long long)(d[n - 1 - i] + 1) : 0ull);
+  for (int j = 0; j < n; j++) { key += (unsigned long long)(v % 10u + 1u) * w; v /= 10u; w *= 11ull; }
   return key;
+}
+
+// A pod's string-order key (include/gshare_b200.h gs_id_split_t): the
+// function's slot for this counter text, then the text itself.
+__device__ __forceinline__ unsigned long long pod_okey(const gs_function_t& fs,
+                                                       const gs_id_split_t* splits, int ctr) {
+  const unsigned long long dk = digits_key(ctr);
+  int slot = fs.id_rank;
+  #pragma unroll 1
+  for (int k = 0; k < fs.n_id_splits; k++) {
+    const gs_id_split_t sp = splits[fs.id_split_off + k];
+    if (dk > sp.threshold) slot = sp.slot;
+  }
+  return (unsigned long long)slot * POW11_10 + dk;
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -165,6 +181,7 @@ struct Ctx {
   const gs_point_t* points;
   const int32_t* counts;
   const gs_init_t* inits;
+  const gs_id_split_t* splits;
   int G, F, P, R, RET, W, T, flags, Q;
   double ws, qs, quantum, cap_mb;
   int lane;
@@ -616,7 +633,7 @@ __device__ int make_pod(Ctx& c, int f, int k, int has_qreq, double qreq, int war
   c.t->p_fn[slot] = f; c.t->p_pt[slot] = k; c.t->p_node[slot] = -1; c.t->p_flags[slot] = PF_ALIVE;
   c.t->p_warm[slot] = warm; c.t->p_ctr[slot] = ctr; c.t->p_x[slot] = 0; c.t->p_y[slot] = 0;
   c.t->p_w[slot] = p.rect_w; c.t->p_h[slot] = p.rect_h; c.t->p_cw[slot] = 0; c.t->p_ci[slot] = 0;
-  c.t->p_okey[slot] = (unsigned long long)c.fs[f].id_rank * POW11_10 + digits_key(ctr);
+  c.t->p_okey[slot] = pod_okey(c.fs[f], c.splits, ctr);
   c.t->p_sm[slot] = p.sm_eff;
   c.t->p_qlim[slot] = p.quota;
   c.t->p_qreq[slot] = has_qreq ? qreq : p.quota;

@@ -1060,7 +1060,6 @@ __device__ void xl_make_pods(Ctx& c, int f, long long n_eff, int ideal, int warm
   if (top < stop) { stop = top; code = GS_ERR_CAPACITY; detail = GS_CAP_PODS; a0 = c.P; a1 = 0; }
   const int made = (int)stop;
   const int ctr0 = c.t->f_pctr[f];
-  const unsigned long long okey0 = (unsigned long long)fs.id_rank * POW11_10;
 #pragma unroll 1
   for (int i = lane; i < made; i += 32) {
     const int k = i < n_eff ? pe : ideal;
@@ -1070,7 +1069,7 @@ __device__ void xl_make_pods(Ctx& c, int f, long long n_eff, int ideal, int warm
     c.t->p_fn[slot] = f; c.t->p_pt[slot] = k; c.t->p_node[slot] = -1; c.t->p_flags[slot] = PF_ALIVE;
     c.t->p_warm[slot] = warm; c.t->p_ctr[slot] = ctr; c.t->p_x[slot] = 0; c.t->p_y[slot] = 0;
     c.t->p_w[slot] = p.rect_w; c.t->p_h[slot] = p.rect_h; c.t->p_cw[slot] = 0; c.t->p_ci[slot] = 0;
-    c.t->p_okey[slot] = okey0 + digits_key(ctr);
+    c.t->p_okey[slot] = pod_okey(fs, c.splits, ctr);
     c.t->p_sm[slot] = p.sm_eff;
     c.t->p_qlim[slot] = p.quota;
     c.t->p_qreq[slot] = p.quota;

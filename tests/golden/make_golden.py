@@ -272,6 +272,52 @@ def error_branch_cases():
     return out
 
 
+PREFIX_FAMILIES = [
+    ["x", "x-005", "x-01a", "x-0", "x-a"],
+    ["m", "m-", "m-005", "m-005-1", "m-1"],
+    ["1", "1-0", "1-007", "1-007-0", "10"],
+    ["bert", "bert-01", "bert-01-a", "bert-015", "bert2"],
+    ["f", "f-0099", "f-0100x", "f-00x"],
+]
+
+
+def prefix_cases(n: int = 40, seed: int = 8675309):
+    """Function ids that extend other ids with "-" (pod-id string order then
+    interleaves the families' pods by counter text, sim_engine.py:354): long,
+    scaling-heavy runs so pod counters cross the thresholds ("x-005" splits
+    the pods of "x" at counter 50, "x-01a" at 200, ...)."""
+    rng = random.Random(seed)
+    out = []
+    for k in range(n):
+        fam = PREFIX_FAMILIES[k % len(PREFIX_FAMILIES)]
+        fids = rng.sample(fam, rng.randint(2, len(fam)))
+        windows = rng.randint(40, 140)
+        fns = []
+        for fid in fids:
+            synth, sms, qs = _synth(rng, True)
+            synth["t_max"] = round(rng.uniform(4, 25), 1)   # small pods: many of them
+            kind = rng.choice(["sinusoid", "step", "constant"])
+            if kind == "sinusoid":
+                tr = {"kind": "sinusoid", "base_rps": round(rng.uniform(10, 60), 1),
+                      "amplitude_rps": round(rng.uniform(10, 50), 1),
+                      "period_windows": rng.randint(4, 30), "poisson": True,
+                      "seed": rng.randint(0, 10 ** 6)}
+            elif kind == "step":
+                tr = {"kind": "step", "base_rps": round(rng.uniform(0, 20), 1),
+                      "step_rps": round(rng.uniform(30, 120), 1),
+                      "step_window": rng.randint(1, windows)}
+            else:
+                tr = {"kind": "constant", "rps": round(rng.uniform(5, 80), 1), "poisson": True}
+            fns.append({"function_id": fid, "profile": {"synth": synth}, "trace": tr,
+                        "initial_pods": [{"sm": rng.choice(sms), "quota": 1.0}]})
+        sc = {"fleet_size": rng.randint(2, 5), "windows": windows,
+              "epoch_windows": rng.randint(1, 3), "cold_start_windows": rng.randint(0, 2),
+              "seed": rng.randint(0, 1000), "gpu_capacity_mb": 81920.0,
+              "restructure_threshold": rng.choice([2, 4, 16]), "functions": fns}
+        out.append({"name": f"prefix-ids-{k:03d}", "scenario": sc, "files": {}})
+    return out
+
+
 def run_reference(case, policy):
     sys.path.insert(0, REF)
     import gshare_sim as ref
@@ -299,6 +345,7 @@ def main(n_random: int = 360, seed: int = 20261017):
     rng = random.Random(seed)
     cases = bundled_cases() + engine_test_cases() + [random_case(rng, i) for i in range(n_random)]
     cases += error_branch_cases()
+    cases += prefix_cases()
     records = []
     for case in cases:
         for policy in ("fast", "timeshare"):

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(backend.LIB_PATH)
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert backend.lib().gs_abi_version() == 1
+    assert backend.lib().gs_abi_version() == 2
 
 
 def test_numpy_structs_match_the_header():

@@ -127,3 +127,22 @@ def test_compile_batch_reports_errors_in_input_order():
     assert len(batch) == 350 and idx == list(range(300)) + list(range(301, 351))
     with pytest.raises(ValueError):
         cc.Batch([batch.images[0]])                    # packed images carry no counts
+
+
+def test_pod_order_keys_follow_pod_id_string_order():
+    """Pod ids f"{fid}-{n:04d}" with ids extending other ids with '-': the
+    device's (slot, digits) key must sort exactly like the strings."""
+    rng = random.Random(11)
+    fams = [["x", "x-1", "x-1-2", "x-10", "x-0100", "x-a", "x-", "x--1", "x-1a", "x-005",
+             "x-01a", "x-0", "x-00", "y", "x-99999999999", "x-1234567890a"],
+            ["1", "1-0", "1-007", "1-007-0", "10", "1-", "1-+", "1- "],
+            ["a", "a+", "a-b", "a-b-c", "a-bc", "é", "a-é", "a-9z"]]
+    for fam in fams:
+        for _ in range(30):
+            fids = rng.sample(fam, rng.randint(1, len(fam)))
+            order = cc._pod_id_order(fids)
+            pods = [(f, n) for f in fids for n in rng.sample(range(0, 200000), 60)
+                    + list(range(0, 120, 7)) + [999, 1000, 1999, 9999, 10000, 99999]]
+            by_str = sorted(pods, key=lambda p: f"{p[0]}-{p[1]:04d}")
+            by_key = sorted(pods, key=lambda p: cc.pod_order_key(order, p[0], p[1]))
+            assert by_str == by_key, fids

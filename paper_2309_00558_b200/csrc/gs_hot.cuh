@@ -569,7 +569,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
           atomicOr(&h->ostate[g], 2);
           atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
         } else {
-          h->covbits[g] = FULL_Q;        // a full quantum is the max (benign race)
+          atomicMax(&h->covbits[g], FULL_Q);   // a full quantum is the max
         }
         grants++;
       }

@@ -103,3 +103,31 @@ def test_gloo_world2_failure_on_one_rank_raises_everywhere(tmp_path):
     assert r0[0].startswith("GShareError: scenario 5 failed on another rank"), r0
     assert r1[0].startswith("ValidationError"), r1
     assert r0[1] == r1[1] == "1"        # one zeroed summary in the gathered array
+
+
+def _worker_nccl(rank, world, port, out_dir):
+    """dist.run_sharded on the GPU with NCCL (world 1: the box has one GPU):
+    the device path, the device-buffer all-gather and the summary records."""
+    import torch
+    import torch.distributed as dist
+    from paper_2309_00558_b200 import engine
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    scen = wl.c2_scenarios(range(40), windows=60)
+    local, summ = gd.run_sharded(scen, "fast")
+    ref = engine.simulate(scen, "fast")
+    same = all(a.report == b.report for a, b in zip(local, ref))
+    recs = np.stack([r.summary for r in ref])
+    with open(os.path.join(out_dir, "nccl.txt"), "w") as fh:
+        fh.write(f"{same} {summ.tobytes() == recs.tobytes()} {len(summ)}\n")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_run_sharded_on_the_gpu_with_nccl(tmp_path):
+    mp.spawn(_worker_nccl, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    assert (tmp_path / "nccl.txt").read_text().split() == ["True", "True", "40"]

@@ -573,9 +573,14 @@ def compile_batch(scenarios, policies, caps: Caps | None = None, *,
     # (and so copy-on-write fault) every object of the parent
     import gc
     gc.freeze()
+    import warnings
     try:
-        with mp.get_context("fork").Pool(workers) as pool:
-            got = pool.map(_forked_part, bounds, chunksize=1)
+        with warnings.catch_warnings():
+            # the workers only run Python/numpy lowering (no CUDA, no threads)
+            warnings.filterwarnings("ignore", message=".*use of fork\\(\\) may lead to deadlocks.*",
+                                    category=DeprecationWarning)
+            with mp.get_context("fork").Pool(workers) as pool:
+                got = pool.map(_forked_part, bounds, chunksize=1)
     finally:
         _FORK_STATE = None
         gc.unfreeze()
@@ -772,7 +777,9 @@ class Batch:
             a = getattr(self, name)
             p = host_empty(len(a), a.dtype)
             p[:len(a)] = a
-            setattr(self, name, p[:len(a)] if len(a) else p)
+            # an empty id_splits must stay empty (its length is part of the
+            # batch shape); the other arrays are never empty
+            setattr(self, name, p[:len(a)] if (len(a) or name == "id_splits") else p)
         return self
 
     def input_bytes(self) -> int:

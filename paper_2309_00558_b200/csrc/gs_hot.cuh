@@ -203,10 +203,10 @@ __device__ __noinline__ void hot_complete_sm(H* h, int lane) {
   #pragma unroll 1
   for (int g = lane; g < h->G; g += 32) {
     double sr = h->sr[g];
+    const int lo = h->seg[g];
     #pragma unroll 1
-    for (int j = h->seg[g]; j < h->seg[g + 1]; j++) {
+    for (int j = lo; j < lo + h->ngr[g]; j++) {       // the granted prefix of the order
       const int i = h->order[j];
-      if (!(h->flags[i] & PF_GRANT)) break;
       sr -= h->sm[i];
       if (sr < 0 && sr > -SM_EPS) sr = 0.0;
     }
@@ -439,11 +439,10 @@ __device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
       PySum occ;
       occ.reset();
       int ng = 0;
-      const int e = h->seg[g + 1];
+      const int e = h->seg[g] + h->reqsm[g];      // the requesting prefix of the order
 #pragma unroll 1
       for (int j = h->seg[g]; j < e; j++) {
         const int i = h->order[j];
-        if (h->key[i] == NOT_REQ) break;          // rest of the node is not requesting
         const double sm = h->sm[i];
         if (sm + sr > SM_LIMIT + SM_EPS) break;
         const double rem = h->qlim[i] - h->qused[i];
@@ -455,6 +454,7 @@ __device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
         ng++;
       }
       h->sr[g] = sr;
+      h->ngr[g] = ng;
       if (ng) {
         h->cov[g] += mx;
         h->occ[g] += occ.value() / 100.0;
@@ -499,8 +499,10 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const bool cand = !(h->qlim[i] - qused <= QUOTA_EPS);
     const bool req = cand && ((fl & PF_CUR) || (h->qlen[f] - h->pinned[f] > 0));
     h->key[i] = req ? -(h->qreq[i] - qused) : NOT_REQ;
-    if (req && integral && h->maycut[h->fnode[i] >> 16])
-      atomicAdd(&h->reqsm[h->fnode[i] >> 16], (int)h->sm[i]);
+    // integral: requesting SM per node (only where it can exceed 100);
+    // otherwise: requesting pods per node (the float dispatch walk's bound)
+    if (req && (!integral || h->maycut[h->fnode[i] >> 16]))
+      atomicAdd(&h->reqsm[h->fnode[i] >> 16], integral ? (int)h->sm[i] : 1);
     any_req |= req;
   }
   // No pod requests a token: dispatch grants nothing, so coverage, occupancy,
@@ -516,14 +518,16 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   // cut is the smallest misfit rank (token_backend.py:169-177).
 #pragma unroll 1
   for (int i = lane; i < n; i += 32) {
-    const int g = h->fnode[i] >> 16;
     const double k = h->key[i];
+    // non-requesting pods are never dispatched: no position needed (the
+    // dispatch walks stop at the requesting / granted prefix of the order)
+    if (k == NOT_REQ) continue;
+    const int g = h->fnode[i] >> 16;
     const int lo = h->seg[g], hi = h->seg[g + 1];
     int r = 0;
     // the SM sum ahead is only needed when the node's requesting SM can
     // exceed 100 (otherwise no requesting pod misfits)
-    const bool need_ahead = integral && k != NOT_REQ && h->maycut[g] &&
-                            h->reqsm[g] > (int)SM_LIMIT;
+    const bool need_ahead = integral && h->maycut[g] && h->reqsm[g] > (int)SM_LIMIT;
     if (need_ahead) {
       double ahead = 0.0;
 #pragma unroll 1
@@ -549,7 +553,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       }
     }
     // (each order position is read and written only by the lane whose pod lands there)
-    if (integral && k != NOT_REQ && (int)h->order[lo + r] != i) atomicOr(&h->ostate[g], 1);
+    if (integral && (int)h->order[lo + r] != i) atomicOr(&h->ostate[g], 1);
     h->order[lo + r] = (unsigned char)i;
     h->rank[i] = (unsigned char)r;
   }

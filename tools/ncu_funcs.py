@@ -21,7 +21,7 @@ for path in glob.glob(os.path.join(CSRC, "*")):
         fn_of[(os.path.basename(path), i)] = cur
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
-cub = glob.glob(tmp + "/*.cubin")[0]
+cub = max(glob.glob(tmp + "/*.cubin"), key=os.path.getsize)
 dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
 secs = re.split(r"\n\s*\.section\s+\.text\.", dis)
 dis = [s for s in secs if s.startswith("_ZN2gs") and "gs_sim_kernel" in s.split(",")[0] and kname in s.split(",")[0]][0]

@@ -11,7 +11,7 @@ rep, so = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
-cubin = glob.glob(os.path.join(tmp, "*.cubin"))[0]
+cubin = max(glob.glob(os.path.join(tmp, "*.cubin")), key=os.path.getsize)
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 line_of = {}
 cur = None

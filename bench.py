@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--no-api", action="store_true", help="skip the e2e_api measurement")
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--configs", default="C1,C3,C4,C5")
+    ap.add_argument("--api-runs", type=int, default=3552,
+                    help="C2 runs of the e2e_api measurement (one wave of resident runs)")
     return ap.parse_args()
 
 
@@ -215,9 +217,13 @@ def oracle_sample(batch, threads: int, target_s: float, n_fixed: int = 0):
 def parity_sample(sub, gpu: dict, ref: dict) -> dict:
     """Record-by-record comparison of the GPU outputs with the oracle's on the
     runs of ``sub`` (a prefix of the GPU batch, identical layout): status
-    (code, decision counters), summary record, function / GPU / global rows,
-    final placements.  Runs the device reported over capacity are rerun with
-    larger capacities by the engine, so they are counted, not compared."""
+    (code, decision counters), summary record, function / GPU / global rows
+    (GPU rows only where the node had placements: the others are not part of
+    the report, sim_engine.py:569-571), and the final placements as a set
+    per run (the report keys them by node and pod id; the record order is
+    not part of the reference's output).  Runs the device reported over
+    capacity are rerun with larger capacities by the engine, so they are
+    counted, not compared."""
     import numpy as np
     from paper_2309_00558_b200 import compiler as cc
     n = len(sub)
@@ -226,15 +232,23 @@ def parity_sample(sub, gpu: dict, ref: dict) -> dict:
     fields = ("code", "token_grants", "scale_decisions", "placement_attempts", "pod_steps",
               "rect_scans", "peak_pods", "n_placements", "detail", "arg0", "arg1")
     ok = np.ones(n, bool)
+    bad_by: dict = {}
+
+    def note(name, good):
+        nonlocal ok
+        k = int((~good & ~cap).sum())
+        if k:
+            bad_by[name] = bad_by.get(name, 0) + k
+        ok &= good
+
     for f in fields:
-        ok &= gs[f] == rs[f]
-    ok &= (gpu["summary"][:n].view(np.uint8).reshape(n, -1)
-           == ref["summary"][:n].view(np.uint8).reshape(n, -1)).all(axis=1)
+        note("status." + f, gs[f] == rs[f])
+    note("summary", (gpu["summary"][:n].view(np.uint8).reshape(n, -1)
+                     == ref["summary"][:n].view(np.uint8).reshape(n, -1)).all(axis=1))
     runs = sub.runs
     for key, off, per in (("fn_rows", "fn_row_off", runs["windows"] * runs["n_funcs"]),
                           ("gpu_rows", "gpu_row_off", runs["windows"] * runs["n_nodes"]),
-                          ("glob_rows", "glob_row_off", runs["windows"]),
-                          ("placements", "place_off", gs["n_placements"])):
+                          ("glob_rows", "glob_row_off", runs["windows"])):
         a, b = gpu[key], ref[key]
         names = [x for x in a.dtype.names if x not in ("pad", "present")]
         end = int(runs[off][-1] + per[-1]) if n else 0
@@ -242,23 +256,30 @@ def parity_sample(sub, gpu: dict, ref: dict) -> dict:
         for x in names:
             eq &= a[x][:end] == b[x][:end]
         if key == "gpu_rows":
-            # rows of nodes without placements are not part of the report
-            # (sim_engine.py:569-571): only their presence flag is compared
             pa, pb = a["present"][:end] != 0, b["present"][:end] != 0
             eq = (pa == pb) & (eq | ~pa)
-        if eq.all():
-            continue
-        for r in np.nonzero(ok)[0]:
-            o, c = int(runs[off][r]), int(per[r])
-            if not eq[o:o + c].all():
-                ok[r] = False
+        good = np.ones(n, bool)
+        if not eq.all():
+            for r in range(n):
+                o, c = int(runs[off][r]), int(per[r])
+                good[r] = bool(eq[o:o + c].all())
+        note(key, good)
+    good = np.ones(n, bool)
+    names = [x for x in gpu["placements"].dtype.names if x != "pad"]
+    for r in np.nonzero(ok)[0]:
+        o, c = int(runs["place_off"][r]), int(gs["n_placements"][r])
+        a = np.sort(gpu["placements"][o:o + c][names], order=names)
+        b = np.sort(ref["placements"][o:o + c][names], order=names)
+        good[r] = bool(np.array_equal(a, b))
+    note("placements", good)
     compared = ~cap
     bad = np.nonzero(compared & ~ok)[0]
     return {"runs": int(compared.sum()), "bit_exact": int((compared & ok).sum()),
             "capacity_reruns_skipped": int(cap.sum()),
             "first_mismatch": int(bad[0]) if len(bad) else None,
-            "fields": "status code/detail + decision counters, summary record, "
-                      "fn/gpu/global rows, placements"}
+            "mismatched_runs_by_record": bad_by,
+            "fields": "status code/detail + decision counters, summary record, fn/gpu/global "
+                      "rows, placements (as a set per run)"}
 
 
 def load_peak():
@@ -331,7 +352,7 @@ def measure_api(args, seeds, dev):
     kernel, D2H and report construction all inside the host wall clock."""
     import torch
     from paper_2309_00558_b200 import engine, workloads as wl
-    scen = wl.c2_scenarios(seeds, windows=args.windows)       # the caller's objects
+    scen = wl.c2_scenarios(list(seeds)[:args.api_runs], windows=args.windows)  # caller's objects
     t0 = time.perf_counter()
     reps = engine.run_batch(scen, "fast", device=dev)
     t1 = time.perf_counter()
@@ -352,8 +373,9 @@ def config_workloads(names, windows_c4: int = 600):
     from paper_2309_00558_b200 import workloads as wl
     out = []
     if "C1" in names:
-        out.append(("C1", "1 node, 3 MLPerf functions, fixed RPS, 60 windows, both policies",
-                    wl.ScenarioSeq(lambda i: wl.c1(), 2048), ["fast", "timeshare"] * 1024))
+        out.append(("C1", "1 node, 3 MLPerf functions, fixed RPS, 60 windows, both policies "
+                          "(4736 copies = one wave of XS warps: 148 SMs x 32)",
+                    wl.ScenarioSeq(lambda i: wl.c1(), 4736), ["fast", "timeshare"] * 2368))
     if "C3" in names:
         out.append(("C3", "FaST-GShare vs time-sharing: 1024 bursty traces x both policies",
                     wl.ScenarioSeq(lambda i: wl.c3(i // 2), 2048), ["fast", "timeshare"] * 1024))

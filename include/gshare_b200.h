@@ -285,6 +285,11 @@ int64_t gs_format_csv(const gs_batch_t* in, const gs_out_t* out, int run,
 int64_t gs_format_csv_batch(const gs_batch_t* in, const gs_out_t* out, int r0, int r1,
                             const char* fid_csv, const int64_t* fid_off, char* buf,
                             int64_t cap, int64_t* offs, int64_t* lens, int n_threads);
+/* summary() inputs of runs [r0, r1): per function (batch order from the
+ * first run's func_off) arrivals, completions, slo_violations, dropped summed
+ * over the windows, and the final queue depth -- 5 int64 per function. */
+int gs_fn_totals(const gs_batch_t* in, const gs_out_t* out, int r0, int r1, int64_t* totals,
+                 int n_threads);
 /* fmt_num(round(x[k], nd)) (nd < 0: fmt_num(x[k])) as NUL-terminated text
  * at buf + k*stride (stride >= 48). */
 int gs_format_numbers(const double* x, int64_t n, int nd, char* buf, int64_t stride);

@@ -71,6 +71,8 @@ def lib():
             L.gs_format_csv.restype = i64
             L.gs_format_csv_batch.argtypes = [vp, vp, i, i, vp, vp, vp, i64, vp, vp, i]
             L.gs_format_csv_batch.restype = i64
+            L.gs_fn_totals.argtypes = [vp, vp, i, i, vp, i]
+            L.gs_fn_totals.restype = i
             L.gs_format_numbers.argtypes = [vp, i64, i, vp, i64]
             L.gs_format_numbers.restype = i
             if L.gs_abi_version() != 2:
@@ -102,19 +104,55 @@ class _HostBlock:
             self.ptr = C.c_void_p()
 
 
-def host_empty(n: int, dtype):
-    """Uninitialised numpy array of ``n`` records in pinned, mapped host memory."""
+def host_empty(n: int, dtype, recycle: bool = False):
+    """Uninitialised numpy array of ``n`` records in pinned, mapped host memory.
+
+    ``recycle``: the block comes from (and, once the last view of it is
+    collected, goes back to) a pool of page-locked blocks, so repeated batch
+    calls do not pay cudaHostAlloc / the page pinning each time."""
     import numpy as np
     dtype = np.dtype(dtype)
-    blk = _HostBlock(max(n, 1) * dtype.itemsize)
-    buf = (C.c_char * blk.nbytes).from_address(blk.ptr.value)
+    nbytes = max(n, 1) * dtype.itemsize
+    if recycle:
+        size = _size_class(nbytes)
+        with _pool_lock:
+            free = _POOL.get(size)
+            blk = free.pop() if free else None
+            if blk is not None:
+                _pool_bytes[0] -= blk.nbytes
+        if blk is None:
+            blk = _HostBlock(size)
+    else:
+        blk = _HostBlock(nbytes)
+    buf = (C.c_char * nbytes).from_address(blk.ptr.value)
     # numpy views keep `buf` alive; `buf` keeps the block alive until collected
     _KEEP[id(buf)] = blk
-    weakref.finalize(buf, _KEEP.pop, id(buf), None)
+    weakref.finalize(buf, _release, id(buf), recycle)
     return np.frombuffer(buf, dtype=dtype, count=max(n, 1))
 
 
 _KEEP: dict = {}
+_POOL: dict = {}                 # block size -> free page-locked blocks
+_pool_lock = threading.RLock()   # re-entrant: a finalizer may run inside the lock
+_pool_bytes = [0]
+_POOL_LIMIT = 8 << 30            # keep at most this much pinned memory idle
+
+
+def _size_class(nbytes: int) -> int:
+    """Pool block size: powers of two up to 64 MiB, then 64 MiB steps."""
+    if nbytes <= (64 << 20):
+        return 1 << max(12, (nbytes - 1).bit_length())
+    return -(-nbytes // (64 << 20)) * (64 << 20)
+
+
+def _release(key, recycle):
+    blk = _KEEP.pop(key, None)
+    if blk is None or not recycle:
+        return                                  # _HostBlock.__del__ frees it
+    with _pool_lock:
+        if _pool_bytes[0] + blk.nbytes <= _POOL_LIMIT:
+            _POOL.setdefault(blk.nbytes, []).append(blk)
+            _pool_bytes[0] += blk.nbytes
 
 
 def run_batch(batch, device: int = 0, rows: bool = True, stream=None, out: dict | None = None) -> dict:

@@ -752,12 +752,16 @@ class Batch:
             b.n_placements = int(last["place_off"]) + int(last["cap_pods"])
         return b
 
-    def alloc_outputs(self, rows: bool = True, pinned: bool = False):
+    def alloc_outputs(self, rows: bool = True, pinned: bool | str = False):
         """Output arrays.  ``pinned=True`` places the row arrays in page-locked,
         device-mapped host memory, which the kernel fills in place (zero-copy,
-        overlapped with the simulation); the contents start uninitialised."""
+        overlapped with the simulation); the contents start uninitialised.
+        ``pinned="pool"``: the same, from the recycled page-locked pool."""
         if pinned:
-            from .backend import host_empty as alloc
+            from .backend import host_empty
+
+            def alloc(n, dt):
+                return host_empty(n, dt, recycle=(pinned == "pool"))
         else:
             def alloc(n, dt):
                 return np.zeros(max(n, 1), dt)

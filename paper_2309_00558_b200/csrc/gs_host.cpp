@@ -208,3 +208,44 @@ extern "C" int gs_format_numbers(const double* x, int64_t n, int nd, char* buf, 
   }
   return 0;
 }
+
+// Per-function totals of runs [r0, r1) for summary() (metrics.py:94-113):
+// for every function of every run, (arrivals, completions, slo_violations,
+// dropped) summed over the windows and the last window's queue depth --
+// written at totals[5 * (funcs[func_off + f] - funcs[runs[r0].func_off]) ...],
+// i.e. in batch function order.  Multithreaded over runs.
+extern "C" int gs_fn_totals(const gs_batch_t* in, const gs_out_t* out, int r0, int r1,
+                            int64_t* totals, int n_threads) {
+  if (!in || !out || !out->fn_rows || !totals || r0 < 0 || r1 > in->n_runs || r0 > r1)
+    return -1;
+  const int n = r1 - r0;
+  if (n == 0) return 0;
+  const int base = in->runs[r0].func_off;
+  const int T = std::max(1, std::min(n_threads > 0 ? n_threads
+                                                  : int(std::thread::hardware_concurrency()), n));
+  auto work = [&](int t) {
+    for (int k = t; k < n; k += T) {
+      const gs_scenario_t& s = in->runs[r0 + k];
+      const int W = s.windows, F = s.n_funcs;
+      const gs_fn_row_t* fn = out->fn_rows + s.fn_row_off;
+      int64_t* o = totals + 5 * (int64_t)(s.func_off - base);
+      for (int f = 0; f < F; ++f) {
+        int64_t a = 0, c = 0, v = 0, d = 0;
+        for (int w = 0; w < W; ++w) {
+          const gs_fn_row_t& x = fn[(int64_t)w * F + f];
+          a += x.arrivals; c += x.completions; v += x.slo_violations; d += x.dropped;
+        }
+        o[5 * f + 0] = a; o[5 * f + 1] = c; o[5 * f + 2] = v; o[5 * f + 3] = d;
+        o[5 * f + 4] = W ? fn[(int64_t)(W - 1) * F + f].queue_depth : 0;
+      }
+    }
+  };
+  if (T == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+  }
+  return 0;
+}

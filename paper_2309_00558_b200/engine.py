@@ -125,7 +125,11 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
             break
         if batch is None:
             batch = cc.Batch([images[i] for i in pending])
-        out = backend.run_batch(batch, device=device, rows=True)
+        # row buffers in recycled page-locked memory: the kernel writes them in
+        # place while it runs (zero-copy), no pageable D2H afterwards
+        pinned = "pool" if batch.n_fn_rows * 20 + batch.n_gpu_rows * 32 < (6 << 30) else False
+        out = backend.run_batch(batch, device=device, rows=True,
+                                out=batch.alloc_outputs(rows=True, pinned=pinned))
         retry = []
         for j, i in enumerate(pending):
             st = out["status"][j]

@@ -221,42 +221,61 @@ def summaries(batch, out: dict, runs=None) -> list:
     runs = list(range(len(batch))) if runs is None else list(runs)
     res: list = [None] * len(runs)
     R = batch.runs
+    totals = None
+    if runs and runs == list(range(runs[0], runs[-1] + 1)):
+        # per-function totals of the whole range by the native reducer
+        import ctypes as C
+        from .abi import make_batch_struct, make_out_struct
+        from .backend import lib
+        f0 = int(R["func_off"][runs[0]])
+        f1 = int(R["func_off"][runs[-1]]) + int(R["n_funcs"][runs[-1]])
+        totals = np.zeros((max(f1 - f0, 1), 5), np.int64)
+        b, o = make_batch_struct(batch), make_out_struct(out)
+        if lib().gs_fn_totals(C.byref(b), C.byref(o), runs[0], runs[-1] + 1,
+                              totals.ctypes.data, 0) != 0:
+            raise ValueError("gs_fn_totals: bad arguments")
     groups: dict = {}
     for k, r in enumerate(runs):
         groups.setdefault((int(R["windows"][r]), int(R["n_funcs"][r])), []).append(k)
     fn_all, gl_all, sm_all = out["fn_rows"], out["glob_rows"], out["summary"]
+    def rows_of(arr, off, per):
+        """(runs, per) records: a zero-copy view when the runs' blocks are
+        consecutive (the usual batch layout), else a gather."""
+        if len(off) and per and np.all(np.diff(off) == per):
+            return arr[int(off[0]): int(off[0]) + len(off) * per].reshape(len(off), per)
+        return arr[off[:, None] + np.arange(per)[None, :]]
+
     for (W, F), ks in groups.items():
         rr = np.array([runs[k] for k in ks])
-        fo = R["fn_row_off"][rr]
-        idx = fo[:, None] + np.arange(W * F)[None, :]
-        fn = fn_all[idx].reshape(len(rr), W, F)
-        tot = {name: fn[name].sum(axis=1).tolist() for name in
-               ("arrivals", "completions", "slo_violations", "dropped")}
-        depth = (fn["queue_depth"][:, -1, :] if W else np.zeros((len(rr), F), np.int32)).tolist()
-        go = R["glob_row_off"][rr]
-        gidx = go[:, None] + np.arange(W)[None, :]
-        gl = gl_all[gidx]
+        if totals is not None:
+            fo = R["func_off"][rr] - f0
+            sums = totals[fo[:, None] + np.arange(F)[None, :]]      # (runs, F, 5)
+            depth = sums[:, :, 4].tolist()
+        else:
+            fn = rows_of(fn_all, R["fn_row_off"][rr], W * F).reshape(len(rr), W, F)
+            # the five int32 columns as one contiguous matrix: one reduction pass
+            cols = np.ascontiguousarray(fn).view(np.int32).reshape(len(rr), W, F, 5)
+            sums = cols.sum(axis=1, dtype=np.int64)                 # (runs, F, 5)
+            depth = (cols[:, -1, :, 4] if W else np.zeros((len(rr), F), np.int32)).tolist()
+        tot = {name: sums[:, :, k].tolist() for k, name in
+               enumerate(("arrivals", "completions", "slo_violations", "dropped"))}
+        gl = rows_of(gl_all, R["glob_row_off"][rr], W)
         peak = (gl["gpus_in_use"].max(axis=1) if W else np.zeros(len(rr), np.int32)).tolist()
         fails = gl["placement_failures"].sum(axis=1).tolist()
         sm = sm_all[rr]
         n_gpu = sm["n_gpu_rows"].tolist()
         su, so = sm["sum_utilization"].tolist(), sm["sum_sm_occupancy"].tolist()
+        images = batch.images
         for j, k in enumerate(ks):
-            r = runs[k]
-            im = batch.images[r]
-            per_function = {}
-            comp_all = viol_all = 0
+            im = images[runs[k]]
             a_, c_, v_, d_, q_ = (tot["arrivals"][j], tot["completions"][j],
                                   tot["slo_violations"][j], tot["dropped"][j], depth[j])
-            for f in range(F):
-                comp, viol = c_[f], v_[f]
-                comp_all += comp
-                viol_all += viol
-                per_function[im.fids[f]] = {
-                    "arrivals": a_[f], "completions": comp, "slo_violations": viol,
-                    "dropped": d_[f], "final_queue_depth": q_[f],
-                    "slo_violation_pct": round(100.0 * viol / comp, 6) if comp else 0.0,
-                }
+            per_function = {
+                fid: {"arrivals": a, "completions": c, "slo_violations": v, "dropped": d,
+                      "final_queue_depth": q,
+                      "slo_violation_pct": round(100.0 * v / c, 6) if c else 0.0}
+                for fid, a, c, v, d, q in zip(im.fids, a_, c_, v_, d_, q_)}
+            comp_all, viol_all = sum(c_), sum(v_)
             n = n_gpu[j]
             res[k] = {
                 "schema_version": SCHEMA_VERSION,

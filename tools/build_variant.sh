@@ -9,5 +9,5 @@ if [ "$REV" = "wt" ]; then SRC=$ROOT; else
   SRC=$(mktemp -d); git -C $ROOT archive $REV paper_2309_00558_b200/csrc include | tar -x -C $SRC; fi
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC \
   -Xcompiler -ffp-contract=off -I $SRC/include "$@" -shared -o $ROOT/variants/$NAME.so \
-  $SRC/paper_2309_00558_b200/csrc/gs_kernel.cu -lcudart
+  $SRC/paper_2309_00558_b200/csrc/gs_kernel.cu $SRC/paper_2309_00558_b200/csrc/gs_host.cpp -lcudart
 echo built variants/$NAME.so

@@ -9,7 +9,7 @@ ap.add_argument("libs", nargs="+")
 ap.add_argument("--windows", type=int, default=600)
 ap.add_argument("--runs", type=int, default=148)
 a = ap.parse_args()
-b = cc.Batch([cc.compile_run(Scenario.from_dict(wl.c4(s, windows=a.windows)), "fast") for s in range(a.runs)])
+b, _, _ = cc.compile_batch(wl.ScenarioSeq(lambda s: wl.c4(s, windows=a.windows), a.runs), ["fast"] * a.runs)
 simsec = float((b.runs["windows"] * b.runs["window_s"]).sum())
 ref = None
 for path in a.libs:

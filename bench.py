@@ -599,7 +599,10 @@ def main():
                 "bound": "issue",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "state_touch_frac": achieved / peak,
-                "traffic": ncu.get("dram_bytes_per_launch"),
+                "traffic": (ncu["dram_bytes_per_run"] * len(batch) if "dram_bytes_per_run" in ncu
+                            else ncu.get("dram_bytes_per_launch")),
+                "traffic_source": f"ncu dram__bytes_read+write ({ncu.get('tag')}, "
+                                  f"{ncu.get('runs_in_capture')} runs) scaled to this batch",
                 "peak_source": peak_src,
                 "model": "SURVEY §8d state-touch bytes per launch / device time, against HBM "
                          "peak; the working set lives in shared memory, so real DRAM traffic "

@@ -2,7 +2,7 @@
 
 The accounting itself -- footprint in resident-insertion order and the
 admission test -- runs inside the device placement kernel
-(csrc/gs_epoch.cuh, ``node_footprint`` / ``admit``), restating
+(csrc/gs_kernel.cuh ``footprint`` / ``admit``, csrc/gs_xlh.cuh ``xl_footprint``), restating
 pkg/src/gshare_sim/memory_model.py:61-88.
 """
 from __future__ import annotations

@@ -146,3 +146,19 @@ def test_pod_order_keys_follow_pod_id_string_order():
             by_str = sorted(pods, key=lambda p: f"{p[0]}-{p[1]:04d}")
             by_key = sorted(pods, key=lambda p: cc.pod_order_key(order, p[0], p[1]))
             assert by_str == by_key, fids
+
+
+def test_vector_poisson_draw_equals_the_scalar_loop():
+    """traces.py draws a trace's Poisson counts as one vector; the reference
+    draws one scalar per window (traces.py:40-42 of pkg/src).  Same stream."""
+    from paper_2309_00558_b200.traces import _rates_to_counts
+    rng = random.Random(5)
+    for _ in range(200):
+        seed = rng.randint(0, 10 ** 9)
+        rates = [max(0.0, rng.uniform(-5, 200)) if rng.random() < 0.9 else 0.0
+                 for _ in range(rng.randint(0, 400))]
+        ws = rng.choice([1.0, 0.5, 0.25, 2.0, 0.1])
+        gen = np.random.default_rng(seed)
+        want = [int(gen.poisson(max(r, 0.0) * ws)) for r in rates]
+        got = _rates_to_counts(rates, ws, True, seed)
+        assert [int(x) for x in got] == want

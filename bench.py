@@ -74,8 +74,8 @@ def parse():
     ap.add_argument("--no-api", action="store_true", help="skip the e2e_api measurement")
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--configs", default="C1,C3,C4,C5")
-    ap.add_argument("--api-runs", type=int, default=3552,
-                    help="C2 runs of the e2e_api measurement (one wave of resident runs)")
+    ap.add_argument("--api-runs", type=int, default=0,
+                    help="C2 runs of the e2e_api measurement (0 = --runs: the timed batch)")
     return ap.parse_args()
 
 
@@ -353,7 +353,8 @@ def measure_api(args, seeds, dev):
     import torch
     from paper_2309_00558_b200 import engine, workloads as wl
     import gc
-    scen = wl.c2_scenarios(list(seeds)[:args.api_runs], windows=args.windows)  # caller's objects
+    n_api = args.api_runs if args.api_runs > 0 else len(list(seeds))
+    scen = wl.c2_scenarios(list(seeds)[:n_api], windows=args.windows)  # caller's objects
     # warm-up call of the same size: the page-locked output pool and the
     # compile pool's first fork are paid here, as by any repeated caller
     warm = engine.run_batch(scen, "fast", device=dev)
@@ -372,7 +373,8 @@ def measure_api(args, seeds, dev):
             "summaries_s": round(t2 - t1, 3),
             "failed_runs": sum(1 for s in sums if not s),
             "api": "engine.run_batch(list[Scenario]) -> MetricsReport per run, then "
-                   "summary() of each (compile + GPU + decode timed)"}
+                   "summary() of each (compile + GPU + decode timed); host lowering, "
+                   "the GPU and the summaries pipelined in 8 blocks"}
 
 
 def config_workloads(names, windows_c4: int = 600):

@@ -596,6 +596,72 @@ def compile_batch(scenarios, policies, caps: Caps | None = None, *,
     return Batch.concat(parts), index, errors
 
 
+def compile_stream(scenarios, policies, caps: Caps | None = None, *,
+                   workers: int | None = None, parts: int | None = None):
+    """``compile_batch`` as a stream: yields ``(batch, index, errors)`` per
+    consecutive block of the inputs, in input order, as soon as the block is
+    lowered -- so a caller can start the GPU on the first blocks while the
+    host cores still lower the rest (``engine.simulate_records``).  ``index``
+    holds absolute input positions.  ``parts`` = number of blocks (default:
+    about 8, never below 64 runs per block)."""
+    import os
+    global _FORK_STATE
+    if not (hasattr(scenarios, "__getitem__") and hasattr(scenarios, "__len__")):
+        scenarios = list(scenarios)
+    policies = list(policies)
+    n = len(scenarios)
+    workers = workers if workers is not None else (os.cpu_count() or 1)
+    n_parts = parts if parts is not None else max(1, min(8, n // 64))
+    blocks = [(n * k // n_parts, n * (k + 1) // n_parts) for k in range(n_parts)]
+    if n < _POOL_MIN_RUNS or workers <= 1:
+        for lo, hi in blocks:
+            res = _compile_span(scenarios, policies, caps, lo, hi)
+            idx = [k for k, r in enumerate(res) if isinstance(r, RunImage)]
+            yield (Batch([res[k] for k in idx]), [lo + k for k in idx],
+                   {lo + k: r for k, r in enumerate(res) if not isinstance(r, RunImage)})
+        return
+    # every block is split across all workers, so the blocks complete one
+    # after another (block 0 first) instead of all at the end
+    per_block = workers
+    spans, owner = [], []
+    for b, (lo, hi) in enumerate(blocks):
+        m = min(per_block, max(1, hi - lo))
+        for k in range(m):
+            spans.append((lo + (hi - lo) * k // m, lo + (hi - lo) * (k + 1) // m))
+            owner.append(b)
+    import multiprocessing as mp
+    import gc
+    import warnings
+    _FORK_STATE = (scenarios, policies, caps)
+    gc.freeze()
+    try:
+        with warnings.catch_warnings():
+            warnings.filterwarnings("ignore", message=".*use of fork\\(\\) may lead to deadlocks.*",
+                                    category=DeprecationWarning)
+            pool = mp.get_context("fork").Pool(workers)
+    finally:
+        _FORK_STATE = None
+        gc.unfreeze()
+    try:
+        got = pool.imap(_forked_part, spans, chunksize=1)
+        cur, acc_parts, acc_index, acc_err = 0, [], [], {}
+        for (lo, _hi), b, (part, res) in zip(spans, owner, got):
+            if b != cur:
+                yield Batch.concat(acc_parts), acc_index, acc_err
+                cur, acc_parts, acc_index, acc_err = b, [], [], {}
+            for k, r in enumerate(res):
+                if isinstance(r, RunImage):
+                    acc_index.append(lo + k)
+                else:
+                    acc_err[lo + k] = r
+            if part is not None:
+                acc_parts.append(part)
+        yield Batch.concat(acc_parts), acc_index, acc_err
+    finally:
+        pool.terminate()
+        pool.join()
+
+
 class Batch:
     """Concatenated RunImages + the ctypes ``gs_batch_t`` pointing at them."""
 

@@ -658,6 +658,8 @@ struct gs_session {
   int blocks_per_sm = 0;
   int xl_bytes = (int)XLH_DYN_BYTES;
   size_t input_bytes = 0;
+  bool async_alloc = false;    // blob from cudaMallocAsync on `ord` (one-shot calls)
+  cudaStream_t ord = nullptr;
 };
 
 extern "C" int gs_abi_version(void) { return GS_ABI_VERSION; }
@@ -675,8 +677,11 @@ extern "C" int gs_set_launch(int warps_per_block, int blocks_per_sm) {
   return 0;
 }
 
-extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t** sess_out,
-                                 char* err, size_t err_len) {
+// `ord`: a stream for stream-ordered allocation and input copies (the one-shot
+// path: no device-wide synchronisation, so one-shot calls from several host
+// threads overlap on the GPU); nullptr = cudaMalloc + synchronous copies.
+static int session_create(const gs_batch_t* in, int device, cudaStream_t ord, bool async_alloc,
+                          gs_session_t** sess_out, char* err, size_t err_len) {
   if (!in || !sess_out || in->n_runs < 0) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
@@ -757,7 +762,10 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   size_t o_counter = slot(8 * sizeof(int));
   size_t o_arena = slot((size_t)(arena_bytes > 0 ? arena_bytes : 16));
   s->blob_bytes = off;
-  cudaError_t e = cudaMalloc(&s->blob, s->blob_bytes);
+  s->async_alloc = async_alloc;
+  s->ord = ord;
+  cudaError_t e = async_alloc ? cudaMallocAsync(&s->blob, s->blob_bytes, ord)
+                              : cudaMalloc(&s->blob, s->blob_bytes);
   if (e != cudaSuccess) {
     char b[256];
     std::snprintf(b, sizeof b, "cudaMalloc(%zu bytes): %s", s->blob_bytes, cudaGetErrorString(e));
@@ -768,7 +776,10 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   char* B = s->blob;
   auto up = [&](size_t o, const void* src, size_t n) -> cudaError_t {
     if (!src || !n) return cudaSuccess;
-    return cudaMemcpy(B + o, src, n, cudaMemcpyHostToDevice);
+    // pageable sources are staged before cudaMemcpyAsync returns; page-locked
+    // ones are read on `ord`, which the one-shot caller synchronises
+    return async_alloc ? cudaMemcpyAsync(B + o, src, n, cudaMemcpyHostToDevice, ord)
+                       : cudaMemcpy(B + o, src, n, cudaMemcpyHostToDevice);
   };
   cudaError_t ce = cudaSuccess;
   if (ce == cudaSuccess) ce = up(o_runs, in->runs, sizeof(gs_scenario_t) * (size_t)in->n_runs);
@@ -783,7 +794,8 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   if (ce == cudaSuccess) ce = up(o_order, order.data(), sizeof(int) * (size_t)R);
   if (ce != cudaSuccess) {
     put_err(err, err_len, cudaGetErrorString(ce));
-    cudaFree(s->blob);
+    if (async_alloc) { cudaFreeAsync(s->blob, ord); cudaStreamSynchronize(ord); }
+    else cudaFree(s->blob);
     delete s;
     return GS_ERR_CUDA;
   }
@@ -810,6 +822,11 @@ extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t*
   cudaEventCreate(&s->ev1);
   *sess_out = s;
   return GS_OK;
+}
+
+extern "C" int gs_session_create(const gs_batch_t* in, int device, gs_session_t** sess_out,
+                                 char* err, size_t err_len) {
+  return session_create(in, device, nullptr, false, sess_out, err, err_len);
 }
 
 // The dynamic shared-memory opt-in is a per-(device, kernel) attribute whose
@@ -1025,7 +1042,10 @@ extern "C" void gs_session_destroy(gs_session_t* s) {
   cudaSetDevice(s->device);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
-  if (s->blob) cudaFree(s->blob);
+  if (s->blob) {
+    if (s->async_alloc) cudaFreeAsync(s->blob, s->ord);
+    else cudaFree(s->blob);
+  }
   delete s;
 }
 
@@ -1073,14 +1093,42 @@ extern "C" void gs_host_free(void* ptr) {
   if (ptr) cudaFreeHost(ptr);
 }
 
+// The one-shot call is stream-ordered end to end: allocation (cudaMallocAsync
+// from the device's memory pool, which keeps its blocks between calls), input
+// copies, the launches, the downloads and the free all go on one stream, and
+// with stream == NULL that stream is a private non-blocking one.  Nothing in it
+// synchronises the device, so concurrent one-shot calls (the drop-in API's
+// pipelined batches, engine.simulate_records) overlap on the GPU.
 extern "C" int gs_run_batch(const gs_batch_t* in, const gs_out_t* out, int device, void* stream,
                             char* err, size_t err_len) {
+  if (!in || !out) { put_err(err, err_len, "bad arguments"); return GS_ERR_ARG; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
+    put_err(err, err_len, "no CUDA device visible");
+    return GS_ERR_CUDA;
+  }
+  CK(cudaSetDevice(device));
+  static std::atomic<unsigned> pool_ready{0};      // bit per device (first 32)
+  if (device < 32 && !(pool_ready.load() & (1u << device))) {
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+      unsigned long long keep = 32ull << 30;       // keep up to 32 GB cached between calls
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_ready.fetch_or(1u << device);
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool own = st == nullptr;
+  if (own) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   gs_session_t* s = nullptr;
-  int rc = gs_session_create(in, device, &s, err, err_len);
-  if (rc != GS_OK) return rc;
-  gs_session_map_host(s, out);     // page-locked row buffers are written in place
-  rc = gs_session_run(s, stream, err, err_len);
-  if (rc == GS_OK) rc = gs_session_download(s, out, stream, err, err_len);
-  gs_session_destroy(s);
+  int rc = session_create(in, device, st, true, &s, err, err_len);
+  if (rc == GS_OK) {
+    gs_session_map_host(s, out);     // page-locked row buffers are written in place
+    rc = gs_session_run(s, st, err, err_len);
+    if (rc == GS_OK) rc = gs_session_download(s, out, st, err, err_len);
+    gs_session_destroy(s);           // cudaFreeAsync on st
+    cudaStreamSynchronize(st);
+  }
+  if (own) cudaStreamDestroy(st);
   return rc;
 }

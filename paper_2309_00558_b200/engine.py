@@ -101,8 +101,20 @@ def _normalise(scenarios, policies):
     return scenarios, policies
 
 
+def _pinned_mode(batch):
+    # row buffers in recycled page-locked memory: the kernel writes them in
+    # place while it runs (zero-copy), no pageable D2H afterwards
+    return "pool" if batch.n_fn_rows * 20 + batch.n_gpu_rows * 32 < (6 << 30) else False
+
+
+def _run_part(batch, device):
+    from . import backend
+    return backend.run_batch(batch, device=device, rows=True,
+                             out=batch.alloc_outputs(rows=True, pinned=_pinned_mode(batch)))
+
+
 def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
-                     caps: cc.Caps | None = None) -> list:
+                     caps: cc.Caps | None = None, on_block=None) -> list:
     """Run a batch of (scenario, policy) pairs on the GPU; raw device records.
 
     Returns one ``(batch, out, r)`` handle per input -- run ``r`` of the
@@ -110,46 +122,46 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
     (``errors="return"``).  Runs that outgrow a static device capacity are
     re-executed on the device with enlarged capacities; nothing is truncated.
     ``decode_run`` / ``report.run_csv`` turn a handle into report rows.
+
+    Host lowering and the GPU are pipelined: ``compiler.compile_stream``
+    yields the batch in consecutive blocks as the host cores finish them, and
+    each block goes to the GPU at once as its own stream-ordered one-shot call
+    (``gs_run_batch`` on a private stream, issued from a host thread, GIL
+    released), so the GPU simulates block k while the host lowers block k+1
+    and the blocks' kernels overlap on the device.  ``on_block(batch, out)``
+    (optional) runs on the calling thread as each block's results arrive,
+    while later blocks are still on the GPU.
     """
-    from . import backend
+    from concurrent.futures import ThreadPoolExecutor
     scenarios, policies = _normalise(scenarios, policies)
     results: list = [None] * len(scenarios)
     images: list = [None] * len(scenarios)
-    batch, pending, failed = cc.compile_batch(scenarios, policies, caps)
+    failed: dict = {}
+    jobs = []
+    with ThreadPoolExecutor(max_workers=16, thread_name_prefix="gs-gpu") as pool:
+        for batch, index, errs in cc.compile_stream(scenarios, policies, caps):
+            failed.update(errs)
+            if len(batch):
+                jobs.append((pool.submit(_run_part, batch, device), batch, index))
+        outs = []
+        for fut, batch, index in jobs:
+            outs.append(fut.result())          # re-raises a backend failure
+            if on_block is not None:
+                on_block(batch, outs[-1])
     for i, exc in sorted(failed.items()):
         if errors == "raise" or not isinstance(exc, ValidationError):
             raise exc
         results[i] = exc
-    for _attempt in range(_MAX_CAP_RETRIES):
+    retry: list = []
+    for (_fut, batch, index), out in zip(jobs, outs):
+        retry += _settle(batch, out, index, scenarios, policies, images, results, errors)
+    pending = retry
+    for _attempt in range(_MAX_CAP_RETRIES - 1):
         if not pending:
             break
-        if batch is None:
-            batch = cc.Batch([images[i] for i in pending])
-        # row buffers in recycled page-locked memory: the kernel writes them in
-        # place while it runs (zero-copy), no pageable D2H afterwards
-        pinned = "pool" if batch.n_fn_rows * 20 + batch.n_gpu_rows * 32 < (6 << 30) else False
-        out = backend.run_batch(batch, device=device, rows=True,
-                                out=batch.alloc_outputs(rows=True, pinned=pinned))
-        retry = []
-        for j, i in enumerate(pending):
-            st = out["status"][j]
-            if int(st["code"]) == cc.GS_ERR_CAPACITY:
-                rr = batch.runs[j]
-                caps_j = cc.Caps(int(rr["cap_pods"]), int(rr["cap_rects"]),
-                                 int(rr["cap_returned"]), int(rr["hot_class"])
-                                 ).grown(int(st["detail"]), int(st["hot_class"]))
-                images[i] = cc.compile_run(scenarios[i], policies[i], caps_j)
-                retry.append(i)
-                continue
-            err = run_error(batch.images[j], st)
-            if err is not None:
-                if errors == "raise":
-                    raise err
-                results[i] = err
-            else:
-                results[i] = (batch, out, j)
-        pending = retry
-        batch = None
+        batch = cc.Batch([images[i] for i in pending])
+        out = _run_part(batch, device)
+        pending = _settle(batch, out, pending, scenarios, policies, images, results, errors)
     for i in pending:
         err = CapacityError("run still exceeds device capacities after "
                             f"{_MAX_CAP_RETRIES} enlargements")
@@ -157,6 +169,34 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
             raise err
         results[i] = err
     return results
+
+
+def _settle(batch, out, index, scenarios, policies, images, results, errors) -> list:
+    """Record each run of a finished block; returns the input positions to
+    re-run with grown capacities (recompiled into ``images``)."""
+    codes = out["status"]["code"]
+    retry = []
+    for j in np.flatnonzero(codes != 0).tolist():
+        i = index[j]
+        st = out["status"][j]
+        if int(st["code"]) == cc.GS_ERR_CAPACITY:
+            rr = batch.runs[j]
+            caps_j = cc.Caps(int(rr["cap_pods"]), int(rr["cap_rects"]),
+                             int(rr["cap_returned"]), int(rr["hot_class"])
+                             ).grown(int(st["detail"]), int(st["hot_class"]))
+            images[i] = cc.compile_run(scenarios[i], policies[i], caps_j)
+            retry.append(i)
+            continue
+        err = run_error(batch.images[j], st)
+        if err is not None:
+            if errors == "raise":
+                raise err
+            results[i] = err
+    again = set(retry)
+    for j, i in enumerate(index):
+        if results[i] is None and i not in again:
+            results[i] = (batch, out, j)
+    return retry
 
 
 def simulate(scenarios, policies="fast", *, device: int = 0, errors: str = "raise",
@@ -178,8 +218,14 @@ def run_batch(scenarios, policies="fast", *, device: int = 0, errors: str = "rai
     until touched, ``to_csv()`` renders natively and ``summary()`` comes from
     one vectorised reduction over the whole batch -- same values, same bytes."""
     from .report import DeviceReport, SharedOutputs
-    recs = simulate_records(scenarios, policies, device=device, errors=errors)
     shared: dict = {}
+
+    def ready(batch, out):
+        # summaries of a finished block, computed while later blocks simulate
+        sh = shared[id(out)] = SharedOutputs(batch, out)
+        sh.prepare()
+
+    recs = simulate_records(scenarios, policies, device=device, errors=errors, on_block=ready)
     reps = []
     for r in recs:
         if isinstance(r, Exception):

@@ -319,6 +319,12 @@ class SharedOutputs:
         self.batch, self.out = batch, out
         self._summaries = None
 
+    def prepare(self) -> None:
+        """Compute every run's summary now (the API does this per block while
+        the next blocks are still on the GPU)."""
+        if self._summaries is None:
+            self._summaries = summaries(self.batch, self.out)
+
     def take_summary(self, r: int) -> dict:
         if self._summaries is None:
             self._summaries = summaries(self.batch, self.out)

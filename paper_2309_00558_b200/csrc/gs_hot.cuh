@@ -26,7 +26,6 @@ namespace gs {
 
 enum : int { GS_CAP_HOT = 5 };   // status detail: working set exceeds the size class
 constexpr double NOT_REQ = __builtin_huge_val();   // key of a pod that requests no token
-constexpr unsigned long long FULL_Q = ~0ull;        // covbits: some token had the full quantum
 
 template <int PC_, int FC_, int GC_>
 struct Hot {
@@ -58,9 +57,12 @@ struct Hot {
   int seg[GC + 1];
   int cut[GC];
   unsigned long long covbits[GC];
-  // per step: requesting SM (integral), grants, 1 = dispatch order changed /
-  // 2 = a partial token; occupancy-sum cache of the last all-quantum step
+  // per step: requesting SM (integral), grants, 2 = a partial token / 4 = a
+  // full-quantum token; occupancy-sum cache of the last all-quantum step
+  // (count occn, value occv; valid while the node's bits of the granted-pod
+  // words gw are those of the previous non-idle step, gwp)
   int reqsm[GC], ngr[GC], ostate[GC], occn[GC];
+  unsigned gw[(PC + 31) / 32], gwp[(PC + 31) / 32];
   int maycut[GC];                  // registered SM on the node can exceed 100 (per hot set)
   double occv[GC];
   int nplaced[GC];
@@ -154,7 +156,10 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->counts = c.counts; h->f_ret = c.t->f_ret; h->f_ring = c.t->f_ring;
     h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
     h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
-    h->integral = c.integral() ? 1 : 0;
+    // integral SM partitions (>= 1) and token durations > QUOTA_EPS keep every
+    // occupancy sum exact in any term order (see hot_step); a quantum below
+    // QUOTA_EPS would void that bound, so it takes the sequential float walk
+    h->integral = (c.integral() && c.quantum >= QUOTA_EPS) ? 1 : 0;
     int bnd = 0;
     for (int f = 0; f < c.F; f++) bnd |= c.fs[f].max_queue >= 0;
     h->bounded = bnd;
@@ -516,6 +521,9 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   // head-blocking cut is decided here too: a requesting pod misfits iff
   // sm + (SM of the requesting pods ahead of it) > 100 + 1e-9, and the node's
   // cut is the smallest misfit rank (token_backend.py:169-177).
+  // In the integral path the order matters for nothing else: a node whose
+  // requesting SM is <= 100 grants every requesting pod, and the occupancy
+  // sum is order-free (below) -- such nodes need no ranks at all.
 #pragma unroll 1
   for (int i = lane; i < n; i += 32) {
     const double k = h->key[i];
@@ -528,6 +536,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     // the SM sum ahead is only needed when the node's requesting SM can
     // exceed 100 (otherwise no requesting pod misfits)
     const bool need_ahead = integral && h->maycut[g] && h->reqsm[g] > (int)SM_LIMIT;
+    if (integral && !need_ahead) { h->rank[i] = 0; continue; }   // granted, cut stays open
     if (need_ahead) {
       double ahead = 0.0;
 #pragma unroll 1
@@ -552,46 +561,71 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
         r += (int)(j < i ? a <= k : a < k);
       }
     }
-    // (each order position is read and written only by the lane whose pod lands there)
-    if (integral && (int)h->order[lo + r] != i) atomicOr(&h->ostate[g], 1);
-    h->order[lo + r] = (unsigned char)i;
+    // (each order position is written only by the lane whose pod lands there;
+    // the integral path keeps no order)
+    if (!integral) h->order[lo + r] = (unsigned char)i;
     h->rank[i] = (unsigned char)r;
   }
   __syncwarp();
   const double quantum = h->quantum;
   int grants = 0;
   if (integral) {
+    // grant: the node's tokens go to order[seg, seg + ngr) in any order (the
+    // occupancy sum below is order-free); a ballot per 32 pods records the
+    // granted set for the occupancy cache
 #pragma unroll 1
-    for (int i = lane; i < n; i += 32) {
-      const int g = h->fnode[i] >> 16;
-      if (h->key[i] != NOT_REQ && h->rank[i] < h->cut[g]) {
-        const double rem = h->qlim[i] - h->qused[i];
-        const double dur = rem < quantum ? rem : quantum;
-        h->flags[i] |= PF_GRANT;
-        atomicAdd(&h->ngr[g], 1);
-        if (rem < quantum) {             // partial token: it may set the max duration
-          atomicOr(&h->ostate[g], 2);
-          atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
-        } else {
-          atomicMax(&h->covbits[g], FULL_Q);   // a full quantum is the max
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int i = j0 + lane;
+      bool gr = false;
+      if (i < n) {
+        const int g = h->fnode[i] >> 16;
+        if (h->key[i] != NOT_REQ && h->rank[i] < h->cut[g]) {
+          const double rem = h->qlim[i] - h->qused[i];
+          h->flags[i] |= PF_GRANT;
+          h->order[h->seg[g] + atomicAdd(&h->ngr[g], 1)] = (unsigned char)i;
+          if (rem < quantum) {             // partial token: it may set the max duration
+            atomicOr(&h->ostate[g], 2);
+            atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(rem));
+          } else {
+            atomicOr(&h->ostate[g], 4);    // a full quantum is the max
+          }
+          gr = true;
+          grants++;
         }
-        grants++;
       }
+      const unsigned b = __ballot_sync(FULL, gr);
+      if (lane == 0) { h->gwp[j0 >> 5] = h->gw[j0 >> 5]; h->gw[j0 >> 5] = b; }
     }
     __syncwarp();
-    // occupancy: Python sum() of sm*duration in dispatch order, per node
+    // occupancy: Python sum() of sm*duration over the node's tokens
+    // (sim_engine.py:516-517).  The reference adds them in dispatch order;
+    // here they are added in grant-slot order, with the same result: every
+    // term is sm * dur with an integer sm in [1, 100] and dur in (1e-9, 1],
+    // so the terms and partial sums lie within 2^7 .. 2^-30 and there are at
+    // most 100 of them.  Each Neumaier error term (f - t) + x is then exact
+    // and a multiple of 2^-82, their running sum c stays below 2^-40 and is
+    // exact too, so f + c is the exact real sum S of the terms and sum()
+    // returns fl(S) -- a function of the multiset of terms alone, not of
+    // their order.
 #pragma unroll 1
     for (int g = lane; g < G; g += 32) {
-      const int ng = h->ngr[g];                // granted = dispatch positions [0, ng)
-      if (ng == 0) { h->occn[g] = -1; continue; }   // order rewritten, cache not refreshed
+      const int ng = h->ngr[g];
+      if (ng == 0) { h->occn[g] = -1; continue; }
       const int st = h->ostate[g];
+      const int lo = h->seg[g], hi = h->seg[g + 1];
+      bool same = !(st & 2) && ng == h->occn[g];
+#pragma unroll 1
+      for (int w = lo >> 5; same && w <= ((hi - 1) >> 5); w++) {
+        const int a = lo - 32 * w, b = hi - 32 * w;
+        const unsigned m = (b >= 32 ? FULL : ((1u << b) - 1u)) & (a > 0 ? ~((1u << a) - 1u) : FULL);
+        same = ((h->gw[w] ^ h->gwp[w]) & m) == 0u;
+      }
       double v;
-      if (st == 0 && ng == h->occn[g]) {
-        v = h->occv[g];   // same pods, same order, all full-quantum tokens: same terms
+      if (same) {
+        v = h->occv[g];   // same granted pods, all full-quantum tokens: same terms
       } else {
         PySum occ;
         occ.reset();
-        const int lo = h->seg[g];
 #pragma unroll 1
         for (int j = lo; j < lo + ng; j++) {
           const int i = h->order[j];
@@ -601,8 +635,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
         h->occv[g] = v;
         h->occn[g] = (st & 2) ? -1 : ng;
       }
-      const unsigned long long cb = h->covbits[g];
-      h->cov[g] += cb == FULL_Q ? quantum : __longlong_as_double((long long)cb);
+      h->cov[g] += (st & 4) ? quantum : __longlong_as_double((long long)h->covbits[g]);
       h->occ[g] += v;
     }
   } else {

@@ -35,7 +35,7 @@ struct HotX {
   int *fbase, *fpicks, *fcomp, *fviol;                 // serve scratch
   // nodes [GC]
   double *sr, *cov, *occ, *fp;
-  int *seg, *cut, *reqsm, *ngr, *nplaced;
+  int *seg, *cut, *reqsm, *ngr, *nplaced, *fullq;   // fullq: a full-quantum token this step
   unsigned long long* covbits;
   // run constants
   const int32_t* counts;
@@ -65,7 +65,7 @@ struct HotX {
 constexpr size_t XLH_DYN_BYTES = 224 * 1024;   // dynamic shared memory per XL CTA (+ ~2 KB static)
 constexpr size_t XLH_POD_BYTES = 9 * 8 + 8 + 4 + 4 * 2 + 4 + 1;   // per registered pod
 constexpr size_t XLH_FN_BYTES = 2 * 8 + 25 * 4 + 4;           // per function (+ loff)
-constexpr size_t XLH_NODE_BYTES = 4 * 8 + 5 * 4 + 8 + 4;      // per node (+ seg)
+constexpr size_t XLH_NODE_BYTES = 4 * 8 + 6 * 4 + 8 + 4;      // per node (+ seg)
 
 // upper bound of the carved size (each of the ~50 arrays may pad by < 16 B)
 __host__ __device__ inline size_t xlh_bytes(int PC, int F, int G) {
@@ -97,7 +97,7 @@ __device__ void xlh_carve(HotX* h, char* base, size_t bytes, int F, int G) {
   h->sr = (double*)take(Gn, 8); h->cov = (double*)take(Gn, 8); h->occ = (double*)take(Gn, 8);
   h->fp = (double*)take(Gn, 8); h->covbits = (unsigned long long*)take(Gn, 8);
   h->seg = (int*)take(Gn, 4); h->cut = (int*)take(Gn, 4); h->reqsm = (int*)take(Gn, 4);
-  h->ngr = (int*)take(Gn, 4); h->nplaced = (int*)take(Gn, 4);
+  h->ngr = (int*)take(Gn, 4); h->nplaced = (int*)take(Gn, 4); h->fullq = (int*)take(Gn, 4);
   h->PC = o <= bytes ? PC : 0;
 }
 
@@ -149,7 +149,8 @@ __device__ bool xlh_load(Ctx& c, HotX* h) {
     h->counts = c.counts; h->f_ret = c.t->f_ret; h->f_ring = c.t->f_ring;
     h->ws = c.ws; h->qs = c.qs; h->quantum = c.quantum;
     h->F = c.F; h->G = c.G; h->T = c.T; h->W = c.W; h->RET = c.RET;
-    h->integral = c.integral() ? 1 : 0;
+    // see hot_load: order-free occupancy sums need durations > QUOTA_EPS
+    h->integral = (c.integral() && c.quantum >= QUOTA_EPS) ? 1 : 0;
   }
   __syncthreads();
 #pragma unroll 1
@@ -283,6 +284,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
         h->sr[g] = sr;
       }
       h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull; h->reqsm[g] = 0; h->ngr[g] = 0;
+      h->fullq[g] = 0;
     }
   }
   __syncthreads();
@@ -314,12 +316,15 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
   // keeps the lanes of a warp (mostly one node) converged; four independent
   // accumulators keep the shared-memory loads in flight.  In the integral
   // path the SM ahead of i is a sum of integer-valued doubles, exact in any
-  // order.
+  // order, and only nodes whose requesting SM exceeds 100 need ranks at all
+  // (the others grant every requesting pod; occupancy sums are order-free,
+  // see hot_step).
 #pragma unroll 1
   for (int i = tid; i < n; i += NT) {
     const double k = h->key[i];
     if (k == NOT_REQ) continue;                // never dispatched: no position needed
     const int g = h->fnode[i] >> 16;
+    if (integral && h->reqsm[g] <= (int)SM_LIMIT) { h->rank[i] = 0; continue; }
     const int lo = h->seg[g], hi = h->seg[g + 1];
     const double* key = h->key;
     int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
@@ -356,7 +361,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
       for (; j < hi; j++) r0 += j < i ? key[j] <= k : key[j] < k;
     }
     const int r = (r0 + r1) + (r2 + r3);
-    h->order[lo + r] = (short)i;
+    if (!integral) h->order[lo + r] = (short)i;
     h->rank[i] = (short)r;
   }
   __syncthreads();
@@ -369,10 +374,13 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
       const int g = h->fnode[i] >> 16;
       if (h->key[i] != NOT_REQ && h->rank[i] < h->cut[g]) {
         const double rem = h->qlim[i] - h->qused[i];
-        const double dur = rem < quantum ? rem : quantum;
         h->flags[i] |= PF_GRANT;
-        atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(dur));
-        atomicAdd(&h->ngr[g], 1);
+        // the node's tokens in grant-slot order (the occupancy sum is
+        // order-free, see hot_step); a full quantum is the max duration,
+        // only partial tokens need the (CAS-loop) 64-bit max
+        h->order[h->seg[g] + atomicAdd(&h->ngr[g], 1)] = (short)i;
+        if (rem < quantum) atomicMax(&h->covbits[g], (unsigned long long)__double_as_longlong(rem));
+        else atomicOr(&h->fullq[g], 1);
         grants++;
       }
     }
@@ -481,6 +489,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
       const int g = x - FP;
       const int ng = h->ngr[g];
       if (ng == 0) continue;
+      // dispatch order (float path) or grant-slot order (integral: order-free)
       PySum occ;
       occ.reset();
       const int lo = h->seg[g];
@@ -489,7 +498,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
         const int i = h->order[j];
         occ.add(h->sm[i] * h->dur(i));
       }
-      h->cov[g] += __longlong_as_double((long long)h->covbits[g]);
+      h->cov[g] += h->fullq[g] ? quantum : __longlong_as_double((long long)h->covbits[g]);
       h->occ[g] += occ.value() / 100.0;
       continue;
     }

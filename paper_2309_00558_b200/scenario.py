@@ -157,8 +157,11 @@ def validate_scenario(sc, memo: dict | None = None) -> None:
         entries = fn.profile.entries
         done = memo is not None and memo.get(("full-quota", id(fn.profile))) is fn.profile
         if not done:
-            for sm in sorted({p.sm_partition for p in entries}):
-                need(_point(sm, 1.0, fn) in entries,
+            # (sm, 1.0) in entries, by field values (ConfigPoint equality is
+            # field-tuple equality; no point objects are built)
+            keys = {(p.sm_partition, p.quota) for p in entries}
+            for sm in sorted({k[0] for k in keys}):
+                need((sm, 1.0) in keys,
                      f"{fid}: profile needs the full-quota point ({sm:g}, 1.0) "
                      f"to derive the serving rate")
             if memo is not None:
@@ -167,13 +170,6 @@ def validate_scenario(sc, memo: dict | None = None) -> None:
             need(init.point in entries,
                  f"{fid}: initial pod point ({init.point.sm_partition:g}, "
                  f"{init.point.quota:g}) is not profiled")
-
-
-def _point(sm, q, fn):
-    """A ConfigPoint of the same class the profile is keyed by (ours or the
-    reference's), so dict membership works for both."""
-    cls = type(next(iter(fn.profile.entries)))
-    return cls(sm, q)
 
 
 @functools.lru_cache(maxsize=4096)

@@ -162,3 +162,22 @@ def test_vector_poisson_draw_equals_the_scalar_loop():
         want = [int(gen.poisson(max(r, 0.0) * ws)) for r in rates]
         got = _rates_to_counts(rates, ws, True, seed)
         assert [int(x) for x in got] == want
+
+
+def test_constant_rate_poisson_draw_equals_the_scalar_loop():
+    """A constant-rate trace is drawn as poisson(lam, size=W): the same stream
+    as the reference's one scalar draw per window (traces.py:40-42 of pkg/src)."""
+    from paper_2309_00558_b200.traces import _rates_to_counts, constant_trace
+    rng = random.Random(11)
+    for _ in range(300):
+        seed = rng.randint(0, 10 ** 9)
+        r = rng.choice([0.0, -0.0, rng.uniform(0, 1), rng.uniform(0, 300), 1e-12])
+        n = rng.randint(0, 400)
+        ws = rng.choice([1.0, 0.5, 0.25, 2.0, 0.1])
+        gen = np.random.default_rng(seed)
+        want = [int(gen.poisson(max(r, 0.0) * ws)) for _ in range(n)]
+        assert [int(x) for x in _rates_to_counts([r] * n, ws, True, seed)] == want
+        if n:
+            assert list(constant_trace(abs(r), n, ws, True, seed).counts) == \
+                [int(gen2) for gen2 in np.random.default_rng(seed).poisson(
+                    [max(abs(r), 0.0) * ws] * n)]

@@ -12,7 +12,7 @@ import pytest
 
 import golden
 import oracle
-from parity import assert_gpu_matches_oracle, diff_results
+from parity import assert_gpu_matches_oracle, diff_results, oracle_results
 from paper_2309_00558_b200 import backend, compiler as cc, engine, workloads as wl
 from paper_2309_00558_b200.scenario import Scenario
 
@@ -101,3 +101,31 @@ def test_gpu_matches_oracle_c2_timeshare_and_mixed_classes():
     scen += [Scenario.from_dict(wl.c4(s, windows=12, n_funcs=80, fleet=40)) for s in range(2)]
     pols = ["fast", "timeshare"] * 8
     assert_gpu_matches_oracle(scen, pols)
+
+
+def test_pipelined_run_batch_matches_oracle_reports():
+    """The drop-in batch API lowers and simulates in overlapping blocks
+    (engine.simulate_records: compile_stream + concurrent stream-ordered
+    one-shot calls): every MetricsReport's CSV and summary equal the oracle's,
+    and a run with a mid-run ValidationError (a zero-throughput CSV profile,
+    autoscaler.py:115-117) comes back as that error in its input position."""
+    from paper_2309_00558_b200.metrics import MetricsReport
+    scen = ([Scenario.from_dict(wl.c2(s, windows=40)) for s in range(300)]
+            + [Scenario.from_dict(wl.c3(s, windows=30)) for s in range(150)]
+            + [Scenario.from_dict(wl.c5(i)) for i in range(0, 1500, 7)])
+    pols = ["fast"] * 300 + ["fast", "timeshare"] * 75 + ["fast"] * (len(scen) - 450)
+    bad = [r for r in golden.records() if "no profiled point has positive throughput"
+           in str(r["expect"].get("message", ""))]
+    assert bad, "golden set lost its zero-throughput error records"
+    scen.insert(333, golden.load_scenario(bad[0]))
+    pols.insert(333, bad[0]["policy"])
+    reps = engine.run_batch(scen, pols, errors="return")
+    want = oracle_results(scen, pols)
+    assert len(reps) == len(want) == len(scen)
+    for k, (got, ref) in enumerate(zip(reps, want)):
+        if isinstance(ref, Exception):
+            assert type(got) is type(ref) and str(got) == str(ref), k
+            continue
+        assert isinstance(got, MetricsReport), (k, got)
+        assert got.to_csv() == ref.report.to_csv(), k
+        assert got.summary() == ref.report.summary(), k

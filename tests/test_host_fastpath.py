@@ -181,3 +181,36 @@ def test_constant_rate_poisson_draw_equals_the_scalar_loop():
             assert list(constant_trace(abs(r), n, ws, True, seed).counts) == \
                 [int(gen2) for gen2 in np.random.default_rng(seed).poisson(
                     [max(abs(r), 0.0) * ws] * n)]
+
+
+@pytest.mark.parametrize("parts,workers", [(1, 4), (3, 2), (8, 4), (5, 1)])
+def test_compile_stream_blocks_concatenate_to_compile_batch(parts, workers):
+    """engine.simulate_records streams the batch in blocks (compiler.compile_stream):
+    the blocks are consecutive, carry absolute input positions, report the same
+    errors as compile_batch and hold byte-identical run images."""
+    good = [wl.ScenarioSeq(lambda i: wl.c5(i * 11), 400)[i] for i in range(400)]
+    bad = Scenario.from_dict(wl.c1())
+    bad.functions[0].initial_pods.append(type(bad.functions[0].initial_pods[0])(
+        type(bad.functions[0].initial_pods[0].point)(13.0, 0.4), None))
+    seq = good[:150] + [bad] + good[150:]
+    pols = ["fast"] * len(seq)
+    ref, ref_idx, ref_err = cc.compile_batch(seq, pols, workers=workers)
+    blocks = list(cc.compile_stream(seq, pols, workers=workers, parts=parts))
+    assert len(blocks) == parts
+    idx = [i for _, ix, _ in blocks for i in ix]
+    err = {k: v for _, _, e in blocks for k, v in e.items()}
+    assert idx == ref_idx and list(err) == list(ref_err) == [150]
+    assert str(err[150]) == str(ref_err[150])
+    joined = cc.Batch.concat([b for b, _, _ in blocks])
+    for name in ("runs", "funcs", "counts", "inits", "names", "id_splits"):
+        got, want = getattr(joined, name), getattr(ref, name)
+        if name == "inits":                        # a trailing pad record is optional
+            got, want = got[:joined.n_inits], want[:ref.n_inits]
+        assert len(got) == len(want), name
+        if got.dtype.names is None:
+            assert np.array_equal(got, want), name
+            continue
+        for field in got.dtype.names:              # field by field (struct padding is undefined)
+            if name == "funcs" and field == "point_off":
+                continue                           # deduplicated point blocks: offsets may differ
+            assert np.array_equal(got[field], want[field]), (name, field)

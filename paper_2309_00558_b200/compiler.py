@@ -182,6 +182,13 @@ def _split_threshold(rest: str) -> int:
 
 
 def _pod_id_order(fids):
+    """``_pod_id_order_of`` of a function-id list (a pure function of the
+    strings, cached: the runs of a sweep share their function ids)."""
+    return _pod_id_order_of(tuple(fids))
+
+
+@lru_cache(maxsize=1024)
+def _pod_id_order_of(fids):
     """Pod-id string order as (first slot, [(threshold, slot)]) per function id.
 
     Pod ids are f"{fid}-{n:04d}" (sim_engine.py:354).  Ids whose "fid-"
@@ -285,8 +292,12 @@ def _default_caps(scenario, fns, lowered) -> Caps:
     per_fn = 0
     for fn, lo in zip(fns, lowered):
         t_eff = _t_eff(lo)
-        counts = _counts_array(fn.trace)[:scenario.windows]
-        peak = (int(counts.max()) if len(counts) else 0) / window_s
+        pk = getattr(fn.trace, "peak", None)
+        if pk is not None:
+            peak = pk(int(scenario.windows)) / window_s
+        else:
+            counts = _counts_array(fn.trace)[:scenario.windows]
+            peak = (int(counts.max()) if len(counts) else 0) / window_s
         # t_eff <= 0: the first scale-up raises (autoscaler.py:115-117), so
         # the function never adds pods beyond its initial ones
         grow = int(math.ceil(1.5 * peak / t_eff)) if t_eff > 0 else 0
@@ -662,39 +673,66 @@ def compile_stream(scenarios, policies, caps: Caps | None = None, *,
         pool.join()
 
 
+def _cat(arrs, dt) -> np.ndarray:
+    """Concatenate many small structured arrays of dtype ``dt`` by their bytes
+    (np.concatenate re-derives the structured dtype promotion per input)."""
+    dt = np.dtype(dt)
+    raw = b"".join((a if a.dtype == dt else a.astype(dt)).tobytes() for a in arrs)
+    return np.frombuffer(raw, dtype=dt).copy()
+
+
 class Batch:
     """Concatenated RunImages + the ctypes ``gs_batch_t`` pointing at them."""
 
     def __init__(self, images: list):
         self.images = images
-        n = len(images)
-        self.runs = np.zeros(n, SCENARIO_DT)
-        f_off = p_off = i_off = c_off = n_off = 0
-        fn_rows = gpu_rows = glob_rows = places = 0
-        funcs, points, inits, counts, names, splits = [], [], [], [], [], []
-        s_off = 0
+        for im in images:
+            if im.counts is None:
+                raise ValueError("this RunImage was packed by compile_batch; "
+                                 "use Batch.prefix() / the batch it came with")
+        if not images:
+            self.runs = np.zeros(0, SCENARIO_DT)
+            self.funcs = np.zeros(0, FUNCTION_DT)
+            self.points = np.zeros(0, POINT_DT)
+            self.inits = np.zeros(1, INIT_DT)
+            self.counts = np.zeros(0, np.int32)
+            self.names = np.zeros(1, np.uint8)
+            self.id_splits = np.zeros(0, ID_SPLIT_DT)
+            self.n_fn_rows = self.n_gpu_rows = self.n_glob_rows = self.n_placements = 0
+            self.n_inits = 0
+            return
+        # per-run records and the run-level offsets, vectorised
+        runs = _cat([im.scen for im in images], SCENARIO_DT)
+        W = runs["windows"].astype(np.int64)
+        nf = runs["n_funcs"].astype(np.int64)
+
+        def excl(x):
+            c = np.cumsum(x)
+            return c - x, int(c[-1])
+
+        runs["func_off"], n_funcs_all = excl(nf)
+        runs["fn_row_off"], self.n_fn_rows = excl(W * nf)
+        runs["gpu_row_off"], self.n_gpu_rows = excl(W * runs["n_nodes"].astype(np.int64))
+        runs["glob_row_off"], self.n_glob_rows = excl(W)
+        runs["place_off"], self.n_placements = excl(runs["cap_pods"].astype(np.int64))
+        self.runs = runs
+        # function records: per-run offsets into inits / counts / names /
+        # id_splits repeated over the run's functions
+        funcs = _cat([im.funcs for im in images], FUNCTION_DT)
+        for field, arrs in (("init_off", [im.inits for im in images]),
+                            ("count_off", [im.counts for im in images]),
+                            ("name_off", [im.names for im in images]),
+                            ("id_split_off", [im.id_splits for im in images])):
+            lens = np.fromiter((len(a) for a in arrs), np.int64, len(arrs))
+            funcs[field] += np.repeat(np.cumsum(lens) - lens, nf)
         # point blocks are deduplicated: by object, then by content
         seen: dict = {}
         by_content: dict = {}
         keep: list = []           # holds the blocks so ids in `seen` stay unique
-        for r, im in enumerate(images):
-            if im.counts is None:
-                raise ValueError("this RunImage was packed by compile_batch; "
-                                 "use Batch.prefix() / the batch it came with")
-            s = im.scen.copy()
-            s["func_off"] = f_off
-            s["fn_row_off"] = fn_rows
-            s["gpu_row_off"] = gpu_rows
-            s["glob_row_off"] = glob_rows
-            s["place_off"] = places
-            W = int(s["windows"][0])
-            fn_rows += W * int(s["n_funcs"][0])
-            gpu_rows += W * int(s["n_nodes"][0])
-            glob_rows += W
-            places += int(s["cap_pods"][0])
-            self.runs[r] = s[0]
-            fc = im.funcs.copy()
-            for fi, block in enumerate(im.point_blocks):
+        points, offs = [], []
+        p_off = 0
+        for im in images:
+            for block in im.point_blocks:
                 off = seen.get(id(block))
                 if off is None:
                     ck = block.tobytes()
@@ -705,34 +743,17 @@ class Batch:
                         p_off += len(block)
                     seen[id(block)] = off
                     keep.append(block)
-                fc["point_off"][fi] = off
-            fc["init_off"] += i_off
-            fc["count_off"] += c_off
-            fc["name_off"] += n_off
-            fc["id_split_off"] += s_off
-            funcs.append(fc)
-            inits.append(im.inits)
-            counts.append(im.counts)
-            names.append(im.names)
-            splits.append(im.id_splits)
-            s_off += len(im.id_splits)
-            f_off += len(fc)
-            i_off += len(im.inits)
-            c_off += len(im.counts)
-            n_off += len(im.names)
-        self.funcs = np.concatenate(funcs) if funcs else np.zeros(0, FUNCTION_DT)
+                offs.append(off)
+        funcs["point_off"] = np.asarray(offs, np.int64)
+        self.funcs = funcs
         self.points = np.concatenate(points) if points else np.zeros(0, POINT_DT)
-        self.inits = (np.concatenate(inits) if inits else np.zeros(0, INIT_DT)).astype(INIT_DT)
-        self.counts = np.ascontiguousarray(np.concatenate(counts) if counts
-                                           else np.zeros(0, np.int32), np.int32)
-        self.names = np.frombuffer(b"".join(names) + b"\0", np.uint8).copy()
-        self.id_splits = np.concatenate(splits) if splits else np.zeros(0, ID_SPLIT_DT)
-        self.n_fn_rows, self.n_gpu_rows = fn_rows, gpu_rows
-        self.n_glob_rows, self.n_placements = glob_rows, places
+        inits = [im.inits for im in images]
+        self.n_inits = sum(len(a) for a in inits)
         # keep at least one element so every pointer is valid
-        if len(self.inits) == 0:
-            self.inits = np.zeros(1, INIT_DT)
-        self.n_inits = sum(len(im.inits) for im in images)
+        self.inits = _cat(inits, INIT_DT) if self.n_inits else np.zeros(1, INIT_DT)
+        self.counts = np.ascontiguousarray(np.concatenate([im.counts for im in images]), np.int32)
+        self.names = np.frombuffer(b"".join(im.names for im in images) + b"\0", np.uint8).copy()
+        self.id_splits = _cat([im.id_splits for im in images], ID_SPLIT_DT)
 
     def __len__(self):
         return len(self.images)

@@ -631,12 +631,11 @@ def compile_stream(scenarios, policies, caps: Caps | None = None, *,
             yield (Batch([res[k] for k in idx]), [lo + k for k in idx],
                    {lo + k: r for k, r in enumerate(res) if not isinstance(r, RunImage)})
         return
-    # every block is split across all workers, so the blocks complete one
-    # after another (block 0 first) instead of all at the end
-    per_block = workers
+    # every block is split across all workers (spans of >= 32 runs), so the
+    # blocks complete one after another (block 0 first) instead of all at the end
     spans, owner = [], []
     for b, (lo, hi) in enumerate(blocks):
-        m = min(per_block, max(1, hi - lo))
+        m = max(1, min(workers, (hi - lo) // 32))
         for k in range(m):
             spans.append((lo + (hi - lo) * k // m, lo + (hi - lo) * (k + 1) // m))
             owner.append(b)

@@ -141,6 +141,9 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
     with ThreadPoolExecutor(max_workers=16, thread_name_prefix="gs-gpu") as pool:
         for batch, index, errs in cc.compile_stream(scenarios, policies, caps):
             failed.update(errs)
+            if any(errors == "raise" or not isinstance(e, ValidationError)
+                   for e in errs.values()):
+                break          # it will be raised: lower and simulate no further blocks
             if len(batch):
                 jobs.append((pool.submit(_run_part, batch, device), batch, index))
         outs = []

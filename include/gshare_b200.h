@@ -212,7 +212,10 @@ typedef struct gs_session gs_session_t;
 int gs_abi_version(void);
 
 /* One-shot: host in -> H2D -> simulate -> D2H -> host out.  `stream` may be
- * NULL (a private stream is used).  Returns the worst per-run code. */
+ * NULL (a private non-blocking stream is used).  Stream-ordered: device memory
+ * comes from the device's default memory pool (cudaMallocAsync; the pool keeps
+ * up to 32 GB cached between calls), so concurrent calls from several host
+ * threads overlap on the GPU.  Returns the worst per-run code. */
 int gs_run_batch(const gs_batch_t* in, const gs_out_t* out, int device, void* stream,
                  char* err, size_t err_len);
 

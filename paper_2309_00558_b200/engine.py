@@ -92,7 +92,10 @@ def decode_run(batch: cc.Batch, r: int, out: dict) -> RunResult:
 
 
 def _normalise(scenarios, policies):
-    scenarios = list(scenarios)
+    # an indexable sequence (e.g. workloads.ScenarioSeq) stays lazy: the
+    # lowering workers build its scenarios themselves
+    if not (hasattr(scenarios, "__getitem__") and hasattr(scenarios, "__len__")):
+        scenarios = list(scenarios)
     if isinstance(policies, str):
         policies = [policies] * len(scenarios)
     policies = list(policies)

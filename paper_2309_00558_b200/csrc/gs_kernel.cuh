@@ -703,7 +703,7 @@ __device__ bool place_pod(Ctx& c, int slot, int g, int4 chosen) {
 }
 
 #ifdef GS_XL_TIMING
-__device__ unsigned long long gs_xl_t[32];   // -DGS_XL_TIMING split (tools/xl_timing.py)
+__device__ unsigned long long gs_xl_t[64];   // -DGS_XL_TIMING split (tools/xl_timing.py)
 #define GS_EPOCH_TIC(v) const long long v = clock64()
 #define GS_EPOCH_ADD(k, d) atomicAdd(&gs_xl_t[k], (unsigned long long)(d))
 #else

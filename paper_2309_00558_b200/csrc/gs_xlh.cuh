@@ -242,9 +242,14 @@ template <bool BND>
 #define GS_PH_INIT() long long ph_t_ = clock64()
 #define GS_PH(k) { const long long now_ = clock64(); \
     if (threadIdx.x == 0) atomicAdd(&gs_xl_t[k], (unsigned long long)(now_ - ph_t_)); ph_t_ = now_; }
+// each warp's busy cycles of phase k (its arrival at the barrier): with the
+// phase time above, the average over warps shows the phase's imbalance
+#define GS_PW(k) { const long long now_ = clock64(); \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&gs_xl_t[32 + (k)], (unsigned long long)(now_ - ph_t_)); }
 #else
 #define GS_PH_INIT()
 #define GS_PH(k)
+#define GS_PW(k)
 #endif
 __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
   const double t0 = (double)w * h->ws + (double)s * h->qs;
@@ -287,6 +292,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
       h->fullq[g] = 0;
     }
   }
+  GS_PW(16);
   __syncthreads();
   GS_PH(16);
   // complete live tokens + filter_pods + requesting -> key
@@ -307,6 +313,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     // integral: requesting SM per node; otherwise: requesting pods per node
     if (req) atomicAdd(&h->reqsm[h->fnode[i] >> 16], integral ? (int)h->sm[i] : 1);
   }
+  GS_PW(17);
   __syncthreads();
   GS_PH(17);
   // build_queue order per node by counting (key, pod index): pods before i
@@ -364,6 +371,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     if (!integral) h->order[lo + r] = (short)i;
     h->rank[i] = (short)r;
   }
+  GS_PW(18);
   __syncthreads();
   GS_PH(18);
   const double quantum = h->quantum;
@@ -384,6 +392,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
         grants++;
       }
     }
+    GS_PW(19);
     GS_PH(19);
   } else {
 #pragma unroll 1
@@ -411,6 +420,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     }
   }
   if (grants) atomicAdd(&xs->grants, grants);
+  GS_PW(20);
   __syncthreads();
   GS_PH(20);
   // serve (sim_engine.py:514-552), pod-parallel as in the per-warp classes:
@@ -434,6 +444,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
   }
 #pragma unroll 1
   for (int f = tid; f < F; f += NT) { h->fcomp[f] = 0; h->fviol[f] = 0; h->fpicks[f] = 0; }
+  GS_PW(21);
   __syncthreads();
   GS_PH(21);
   // 2. dry runs (chunk per thread so the block scan below runs in gl order)
@@ -461,6 +472,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     atomicAdd(&h->fpicks[f], p);
     run += p;
   }
+  GS_PW(22);
   __syncthreads();
   GS_PH(22);
   // 4. replay with the pod's FIFO position inside its function
@@ -478,6 +490,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     if (comp) atomicAdd(&h->fcomp[f], comp);
     if (viol) atomicAdd(&h->fviol[f], viol);
   }
+  GS_PW(23);
   __syncthreads();
   GS_PH(23);
   // 5. each function's queue bookkeeping once; on other threads, each node's
@@ -512,6 +525,7 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
     // step's critical path
     if (s + 1 < h->T) hot_admit<HotX, BND>(h, f, (double)w * h->ws + (double)(s + 1) * h->qs);
   }
+  GS_PW(24);
   __syncthreads();
   GS_PH(24);
 }

@@ -8,7 +8,7 @@ from paper_2309_00558_b200.scenario import Scenario
 backend.LIB_PATH = sys.argv[1]
 b = cc.Batch([cc.compile_run(Scenario.from_dict(wl.c4(s, windows=int(os.environ.get("XLT_WINDOWS", "100")))), "fast") for s in range(16)])
 s = backend.Session(b); ms = s.run()
-t = (C.c_ulonglong * 32)()
+t = (C.c_ulonglong * 64)()
 backend.lib().gs_xl_timing(t)
 tot = sum(t[:4])
 print(f"{ms:.1f} ms; warp-0 cycles: epoch {t[0]/tot:.2%} window_begin {t[1]/tot:.2%} steps {t[2]/tot:.2%} window_close {t[3]/tot:.2%}")
@@ -22,3 +22,6 @@ names = ["admit+reset", "complete+key", "rank", "grant", "cov/occ|dispatch", "co
 print("  xlh_step phases: " + "  ".join(f"{nm} {t[16+i]/max(st,1):.1%}" for i, nm in enumerate(names)))
 print(f"  steps {t[25]}  cycles/step {st/max(t[25],1):.0f}  pods/step {t[26]/max(t[25],1):.0f}  granted/step {t[27]/max(t[25],1):.0f}")
 print(f"  max pods on one node: mean over steps {t[28]/max(t[25],1):.0f}, overall max {t[29]}")
+nw = 16   # warps per XL CTA
+print("  per-phase warp efficiency (mean warp busy / phase time; 1 = balanced): " + "  ".join(
+    f"{nm} {t[48 + i] / nw / max(t[16 + i], 1):.2f}" for i, nm in enumerate(names)))

@@ -298,6 +298,32 @@ def load_ncu():
         return {}
 
 
+NCU_CLASSES = os.path.join(ROOT, "profiles", "r2", "ncu_r2g.json")
+
+
+def class_issue(classes):
+    """ncu evidence (profiles/r2/ncu_r2g.json) of the kernel class a config ran
+    in: issue-slot use, IPC, SIMT efficiency, warps active, top stalls."""
+    try:
+        with open(NCU_CLASSES) as fh:
+            caps = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    key = {1: "xs", 2: "s", 5: "xl"}.get(max(classes, key=classes.get) if classes else 0)
+    c = caps.get(key)
+    if c is None:
+        return None
+    m = c["metrics"]
+    return {"source": f"ncu --set full ({c['report']}, {c['runs_in_capture']} runs)",
+            "issue_active_pct": _pct(m.get("smsp__issue_active.avg.pct_of_peak_sustained_active")),
+            "ipc_per_sm": _pct(m.get("sm__inst_executed.avg.per_cycle_active")),
+            "simt_efficiency": (_pct(m.get("smsp__thread_inst_executed_per_inst_executed.ratio"))
+                                or 0) / 32,
+            "warps_active_pct": _pct(m.get("sm__warps_active.avg.pct_of_peak_sustained_active")),
+            "top_stalls": dict(list(c["stall_share"].items())[:3]),
+            "dram_bytes_per_run": c["dram_bytes_per_run"]}
+
+
 def _pct(s):
     try:
         return float(str(s).split()[0])
@@ -426,6 +452,7 @@ def measure_config(name, desc, scen, pols, flush, threads, peak):
             "decisions_per_sec": float((st["token_grants"] + st["scale_decisions"]
                                         + st["placement_attempts"]).sum()) / dev_s,
             "state_touch_frac": algorithmic_bytes(batch, st, out["summary"]) / dev_s / 1e9 / peak,
+            "bound": "issue", "issue": class_issue(classes),
             "size_classes": classes,
             "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"first {len(sub)} runs, {dt:.2f} s"},

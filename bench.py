@@ -18,18 +18,19 @@ A "step" = one launch of the scenario megakernel over the GPU's whole batch.
              host memory (written in place by the kernel into page-locked
              buffers) plus the status/summary D2H -- host wall clock, max
              over ranks.
-``e2e_api``= the drop-in Python API end to end: ``engine.run_batch`` on the
-             list of Scenario objects -> one MetricsReport per run, and
-             ``summary()`` of every report: host compile, H2D, kernel, D2H
-             and report construction inside the timing (N=1, rank 0).
+``e2e_api``= the drop-in Python API end to end on the same batch:
+             ``engine.run_batch`` on the list of Scenario objects -> one
+             MetricsReport per run, and ``summary()`` of every report: host
+             lowering, H2D, kernel, D2H and report construction inside the
+             timing, after one warm-up call of the same size (N=1, rank 0).
 ``parity_sample`` = the oracle (oracle/, a C restatement of pkg/src/gshare_sim
              pinned to the reference's own outputs) re-simulates a prefix of
              the timed runs; every record (rows, placements, decision
              counters, summary) is compared with the GPU's.  At N=1 the same
              oracle pass is timed as ``cpu_baseline``.
 ``per_config`` = the same measurement (device value, state-touch fraction,
-             CPU baseline, parity sample) for the other BASELINE configs
-             C1, C3, C4, C5 (N=1).
+             the kernel class's ncu issue evidence, CPU baseline, parity
+             sample) for the other BASELINE configs C1, C3, C4, C5 (N=1).
 ``--impl reference`` times the CPU oracle port on all host cores on a
 bounded sample of the same workload.
 """

@@ -107,12 +107,36 @@ __host__ __device__ constexpr bool fits(int n_reg, int F, int G) {
   return n_reg <= H::PC && F <= H::FC && G <= H::GC;
 }
 
+// compile-time capacities of a working-set type (HotX, the XL class's
+// runtime-sized view, specialises this with "unbounded")
+template <class H>
+struct HotCap {
+  static constexpr int PC = H::PC, FC = H::FC, GC = H::GC;
+};
+
+// loop bound of a warp-uniform 32-wide sweep over n <= CAP items: with
+// CAP <= 32 at most one trip, known at compile time
+template <int CAP>
+__device__ __forceinline__ int trips32(int n) { return CAP <= 32 ? (n > 0 ? 1 : 0) : n; }
+
+// fn(x) for x = lane, lane + 32, ... < n; a class whose capacity CAP fits one
+// warp needs no loop (one predicated call, no back edge)
+template <int CAP, class Fn>
+__device__ __forceinline__ void lane_for(int lane, int n, Fn&& fn) {
+  if constexpr (CAP <= 32) {
+    if (lane < n) fn(lane);
+  } else {
+#pragma unroll 1
+    for (int x = lane; x < n; x += 32) fn(x);
+  }
+}
+
 // ---------------------------------------------------------------- load/store
 template <class H>
 __device__ bool hot_load(Ctx& c, H* h) {
   const int n = c.sh->n_reg;
   if (n > H::PC || c.F > H::FC || c.G > H::GC) return false;   // window runs on the arena
-  for (int i = c.lane; i < n; i += 32) {
+  lane_for<H::PC>(c.lane, n, [&](int i) {
     int s = c.t->s_rl[i];
     h->qused[i] = c.t->p_qused[s];
     h->qreq[i] = c.t->p_qreq[s];
@@ -126,8 +150,8 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->fnode[i] = c.t->p_fn[s] | (c.t->p_node[s] << 16);
     h->flags[i] = (unsigned char)(c.t->p_flags[s] & PF_CUR);
     h->order[i] = (unsigned char)i;
-  }
-  for (int f = c.lane; f < c.F; f += 32) {
+  });
+  lane_for<H::FC>(c.lane, c.F, [&](int f) {
     h->qlen[f] = c.t->f_qlen[f]; h->pinned[f] = c.t->f_pinned[f];
     h->fw[f] = c.t->f_fw[f]; h->fi[f] = c.t->f_fi[f]; h->fcnt[f] = c.t->f_fn[f];
     h->nsn[f] = c.t->f_nsn[f]; h->nsw[f] = c.t->f_nsw[f]; h->nsi[f] = c.t->f_nsi[f];
@@ -140,7 +164,7 @@ __device__ bool hot_load(Ctx& c, H* h) {
     h->farr[f] = h->fcnt[f] > 0 ? arrival_time(c, f, h->fw[f], h->fi[f]) : 0.0;
     h->fwn[f] = h->fcnt[f] > 0 ? c.count(f, h->fw[f]) : 1;
     h->nswn[f] = (h->nsn[f] > 0 && c.fs[f].max_queue < 0) ? c.count(f, h->nsw[f]) : 1;
-  }
+  });
   for (int f = c.lane; f <= c.F; f += 32) h->loff[f] = c.t->f_loff[f];
   for (int g = c.lane; g < c.G; g += 32) {
     h->sr[g] = c.t->n_sr[g]; h->cov[g] = 0.0; h->occ[g] = 0.0; h->occn[g] = -1;
@@ -177,7 +201,7 @@ __device__ bool hot_load(Ctx& c, H* h) {
 template <class H>
 __device__ void hot_store(Ctx& c, H* h) {
   const int n = h->n;
-  for (int i = c.lane; i < n; i += 32) {
+  lane_for<H::PC>(c.lane, n, [&](int i) {
     int s = c.t->s_rl[i];
     c.t->p_qused[s] = h->qused[i];
     c.t->p_busy[s] = h->busy[i];
@@ -186,14 +210,14 @@ __device__ void hot_store(Ctx& c, H* h) {
     c.t->p_cw[s] = id_w(h->cur[i]);
     c.t->p_ci[s] = id_i(h->cur[i]);
     c.t->p_flags[s] = (c.t->p_flags[s] & ~(PF_CUR | PF_GRANT)) | (h->flags[i] & PF_CUR);
-  }
-  for (int f = c.lane; f < c.F; f += 32) {
+  });
+  lane_for<H::FC>(c.lane, c.F, [&](int f) {
     c.t->f_qlen[f] = h->qlen[f]; c.t->f_pinned[f] = h->pinned[f];
     c.t->f_fw[f] = h->fw[f]; c.t->f_fi[f] = h->fi[f]; c.t->f_fn[f] = h->fcnt[f];
     c.t->f_nsn[f] = h->nsn[f]; c.t->f_nsw[f] = h->nsw[f]; c.t->f_nsi[f] = h->nsi[f];
     c.t->f_rhead[f] = h->rhead[f]; c.t->f_retn[f] = h->retn[f];
     c.t->f_hn[f] = h->hn[f];
-  }
+  });
   for (int g = c.lane; g < c.G; g += 32) c.t->n_sr[g] = h->sr[g];
   __syncwarp();
 }
@@ -226,14 +250,13 @@ __device__ __forceinline__ void hot_complete(H* h, int lane) {
     hot_complete_sm(h, lane);
     __syncwarp();
   }
-  #pragma unroll 1
-  for (int i = lane; i < n; i += 32) {
+  lane_for<H::PC>(lane, n, [&](int i) {
     const int fl = h->flags[i];
     if (fl & PF_GRANT) {
       h->qused[i] += h->dur(i);
       h->flags[i] = (unsigned char)(fl & ~PF_GRANT);
     }
-  }
+  });
 }
 
 template <class H, bool BND>
@@ -478,20 +501,17 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   constexpr bool integral = INTEG;
   // _admit_arrivals touches only queues and _complete_live_tokens only the
   // ledger, so admission runs first and completion fuses with the key pass.
-#pragma unroll 1
-  for (int f = lane; f < F; f += 32) hot_admit<H, BND>(h, f, t0);
+  lane_for<H::FC>(lane, F, [&](int f) { hot_admit<H, BND>(h, f, t0); });
   if (s > 0 && !integral) hot_complete_sm(h, lane);
-#pragma unroll 1
-  for (int g = lane; g < G; g += 32) {
+  lane_for<H::GC>(lane, G, [&](int g) {
     h->cut[g] = 0x7fffffff; h->covbits[g] = 0ull;
     h->reqsm[g] = 0; h->ngr[g] = 0; h->ostate[g] = 0;
-  }
+  });
   __syncwarp();
   // complete live tokens + filter_pods + requesting:
   // key = -(q_req - q_used) for requesting pods, ~0 otherwise
   bool any_req = false;
-#pragma unroll 1
-  for (int i = lane; i < n; i += 32) {
+  lane_for<H::PC>(lane, n, [&](int i) {
     const int f = h->fnode[i] & 0xffff;
     int fl = h->flags[i];
     double qused = h->qused[i];
@@ -509,7 +529,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     if (req && (!integral || h->maycut[h->fnode[i] >> 16]))
       atomicAdd(&h->reqsm[h->fnode[i] >> 16], integral ? (int)h->sm[i] : 1);
     any_req |= req;
-  }
+  });
   // No pod requests a token: dispatch grants nothing, so coverage, occupancy,
   // sm_running and every queue stay as they are (token_backend.py:160-187,
   // sim_engine.py:514-520 iterate over no tokens).
@@ -524,19 +544,18 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   // In the integral path the order matters for nothing else: a node whose
   // requesting SM is <= 100 grants every requesting pod, and the occupancy
   // sum is order-free (below) -- such nodes need no ranks at all.
-#pragma unroll 1
-  for (int i = lane; i < n; i += 32) {
+  lane_for<H::PC>(lane, n, [&](int i) {
     const double k = h->key[i];
     // non-requesting pods are never dispatched: no position needed (the
     // dispatch walks stop at the requesting / granted prefix of the order)
-    if (k == NOT_REQ) continue;
+    if (k == NOT_REQ) return;
     const int g = h->fnode[i] >> 16;
     const int lo = h->seg[g], hi = h->seg[g + 1];
     int r = 0;
     // the SM sum ahead is only needed when the node's requesting SM can
     // exceed 100 (otherwise no requesting pod misfits)
     const bool need_ahead = integral && h->maycut[g] && h->reqsm[g] > (int)SM_LIMIT;
-    if (integral && !need_ahead) { h->rank[i] = 0; continue; }   // granted, cut stays open
+    if (integral && !need_ahead) { h->rank[i] = 0; return; }   // granted, cut stays open
     if (need_ahead) {
       double ahead = 0.0;
 #pragma unroll 1
@@ -565,7 +584,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     // the integral path keeps no order)
     if (!integral) h->order[lo + r] = (unsigned char)i;
     h->rank[i] = (unsigned char)r;
-  }
+  });
   __syncwarp();
   const double quantum = h->quantum;
   int grants = 0;
@@ -574,7 +593,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     // occupancy sum below is order-free); a ballot per 32 pods records the
     // granted set for the occupancy cache
 #pragma unroll 1
-    for (int j0 = 0; j0 < n; j0 += 32) {
+    for (int j0 = 0; j0 < trips32<H::PC>(n); j0 += 32) {
       const int i = j0 + lane;
       bool gr = false;
       if (i < n) {
@@ -607,10 +626,9 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     // exact too, so f + c is the exact real sum S of the terms and sum()
     // returns fl(S) -- a function of the multiset of terms alone, not of
     // their order.
-#pragma unroll 1
-    for (int g = lane; g < G; g += 32) {
+    lane_for<H::GC>(lane, G, [&](int g) {
       const int ng = h->ngr[g];
-      if (ng == 0) { h->occn[g] = -1; continue; }
+      if (ng == 0) { h->occn[g] = -1; return; }
       const int st = h->ostate[g];
       const int lo = h->seg[g], hi = h->seg[g + 1];
       bool same = !(st & 2) && ng == h->occn[g];
@@ -637,7 +655,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       }
       h->cov[g] += (st & 4) ? quantum : __longlong_as_double((long long)h->covbits[g]);
       h->occ[g] += v;
-    }
+    });
   } else {
     grants = hot_dispatch_float(h, lane);
   }
@@ -646,15 +664,14 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   // node, pod_id) order; a dry run counts each pod's request starts, a
   // segmented scan per function turns them into FIFO positions, and a replay
   // serves exactly the requests the sequential drain would have handed out.
-#pragma unroll 1
-  for (int f = lane; f < F; f += 32) {
+  lane_for<H::FC>(lane, F, [&](int f) {
     h->favail[f] = h->retn[f] + h->nsn[f];
     h->fcarry[f] = 0; h->fcomp[f] = 0; h->fviol[f] = 0;
-  }
+  });
   __syncwarp();
   int ngl = 0;
 #pragma unroll 1
-  for (int j0 = 0; j0 < n; j0 += 32) {
+  for (int j0 = 0; j0 < trips32<H::PC>(n); j0 += 32) {
     const int j = j0 + lane;
     const int i = j < n ? h->flist[j] : 0;
     const bool gr = j < n && (h->flags[i] & PF_GRANT);
@@ -665,7 +682,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   __syncwarp();
   const double ws = h->ws;
 #pragma unroll 1
-  for (int k0 = 0; k0 < ngl; k0 += 32) {
+  for (int k0 = 0; k0 < trips32<H::PC>(ngl); k0 += 32) {
     const int k = k0 + lane;
     const bool act = k < ngl;
     const int i = act ? h->rank[k] : 0;
@@ -695,10 +712,9 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     __syncwarp();
   }
   // apply each function's queue bookkeeping once
-#pragma unroll 1
-  for (int f = lane; f < F; f += 32) {
+  lane_for<H::FC>(lane, F, [&](int f) {
     const int want = h->fcarry[f];
-    if (want == 0 && h->fcomp[f] == 0) continue;
+    if (want == 0 && h->fcomp[f] == 0) return;
     const int avail = h->favail[f];
     const int taken = want < avail ? want : avail;
     const int retn = h->retn[f];
@@ -729,7 +745,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     h->qlen[f] -= comp;
     h->wcomp[f] += comp;
     h->wviol[f] += h->fviol[f];
-  }
+  });
   __syncwarp();
   return grants;
 }
@@ -762,10 +778,8 @@ __device__ long long hot_steps(H* h, int lane, int w) {
 // up): reset_window + _generate_arrivals directly on the shared-memory set.
 template <class H>
 __device__ void hot_begin_light(H* h, int lane, int w) {
-#pragma unroll 1
-  for (int i = lane; i < h->n; i += 32) h->qused[i] = 0.0;
-#pragma unroll 1
-  for (int f = lane; f < h->F; f += 32) {
+  lane_for<H::PC>(lane, h->n, [&](int i) { h->qused[i] = 0.0; });
+  lane_for<H::FC>(lane, h->F, [&](int f) {
     const int n = h->count(f, w);
     h->warr[f] = n;
     if (n > 0) {
@@ -775,9 +789,8 @@ __device__ void hot_begin_light(H* h, int lane, int w) {
       }
       h->fcnt[f] += n;
     }
-  }
-#pragma unroll 1
-  for (int g = lane; g < h->G; g += 32) { h->cov[g] = 0.0; h->occ[g] = 0.0; }
+  });
+  lane_for<H::GC>(lane, h->G, [&](int g) { h->cov[g] = 0.0; h->occ[g] = 0.0; });
   __syncwarp();
 }
 

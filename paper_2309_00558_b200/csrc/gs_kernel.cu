@@ -138,8 +138,7 @@ template <class H>
 __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, PySum& su,
                           PySum& so, int& peak, int& fail_total) {
   const gs_scenario_t& sc = *c.sc;
-  #pragma unroll 1
-  for (int f = c.lane; f < c.F; f += 32) {
+  lane_for<HotCap<H>::FC>(c.lane, c.F, [&](int f) {
     const int hn = h->hn[f];
     c.t->f_hist[3 * f + hn % 3] = (double)h->warr[f] / c.ws;   // history.append(n / W)
     h->hn[f] = hn + 1;
@@ -154,10 +153,9 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
     acc.violations += h->wviol[f]; acc.dropped += h->wdrop[f];
     if (w == c.W - 1) acc.final_depth += depth;
     h->wcomp[f] = 0; h->wviol[f] = 0; h->wdrop[f] = 0;
-  }
+  });
   int in_use = 0;
-  #pragma unroll 1
-  for (int g = c.lane; g < c.G; g += 32) {
+  lane_for<HotCap<H>::GC>(c.lane, c.G, [&](int g) {
     gs_gpu_row_t r;
     r.present = h->nplaced[g] > 0 ? 1 : 0;
     r.pad = 0;
@@ -167,7 +165,7 @@ __device__ void hot_close(Ctx& c, H* h, int w, const gs_out_t& out, Accum& acc, 
     r.memory_mb = r.present ? h->fp[g] : 0.0;
     if (out.gpu_rows) out.gpu_rows[sc.gpu_row_off + (long long)w * c.G + g] = r;
     in_use += r.present;
-  }
+  });
   in_use = warp_sum_i(in_use);
   __syncwarp();
   if (c.lane == 0) {

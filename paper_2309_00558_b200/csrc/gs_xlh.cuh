@@ -62,6 +62,11 @@ struct HotX {
   }
 };
 
+template <>
+struct HotCap<HotX> {
+  static constexpr int PC = 1 << 30, FC = 1 << 30, GC = 1 << 30;
+};
+
 constexpr size_t XLH_DYN_BYTES = 224 * 1024;   // dynamic shared memory per XL CTA (+ ~2 KB static)
 constexpr size_t XLH_POD_BYTES = 9 * 8 + 8 + 4 + 4 * 2 + 4 + 1;   // per registered pod
 constexpr size_t XLH_FN_BYTES = 2 * 8 + 25 * 4 + 4;           // per function (+ loff)

@@ -492,7 +492,7 @@ __device__ __noinline__ int hot_dispatch_float(H* h, int lane) {
   return grants;
 }
 
-// returns the token grants of this step (same value in every lane)
+// returns this lane's token grants of the step (hot_steps_t sums the warp once a window)
 template <class H, bool INTEG, bool BND>
 __device__ int hot_step(H* h, int lane, int w, int s) {
   const double t0 = (double)w * h->ws + (double)s * h->qs;
@@ -659,7 +659,6 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
   } else {
     grants = hot_dispatch_float(h, lane);
   }
-  grants = warp_sum_i(grants);
   // serve (sim_engine.py:514-520), pod-parallel.  Granted pods in (function,
   // node, pod_id) order; a dry run counts each pod's request starts, a
   // segmented scan per function turns them into FIFO positions, and a replay
@@ -756,12 +755,12 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
 template <class H, bool INTEG, bool BND>
 __device__ __noinline__ long long hot_steps_t(H* h, int lane, int w) {
   const int T = h->T;
-  long long grants = 0;
+  int grants = 0;              // this lane's grants of the window (< 2^31)
   #pragma unroll 1
   for (int s = 0; s < T; s++) grants += hot_step<H, INTEG, BND>(h, lane, w, s);
   hot_complete(h, lane);
   __syncwarp();
-  return grants;
+  return warp_sum_i(grants);
 }
 
 template <class H>

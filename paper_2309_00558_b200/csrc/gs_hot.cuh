@@ -452,6 +452,30 @@ __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start,
   h->flags[i] = (unsigned char)fl;
 }
 
+// Python sum() of sm * duration over the tokens order[lo, lo + ng) (ng >= 1).
+// One term: 0 + x = x.  Two terms: Neumaier's compensation is the exact
+// rounding error of x1 + x2, so sum() returns fl(x1 + x2) itself; longer
+// sums take the compensated loop.  (Terms are positive: no -0.0 cases.)
+template <class H>
+__device__ __forceinline__ double token_occupancy(const H* h, int lo, int ng) {
+  const int i0 = h->order[lo];
+  const double x0 = h->sm[i0] * h->dur(i0);
+  if (ng == 1) return x0;
+  const int i1 = h->order[lo + 1];
+  const double x1 = h->sm[i1] * h->dur(i1);
+  if (ng == 2) return x0 + x1;
+  PySum occ;
+  occ.reset();
+  occ.add(x0);
+  occ.add(x1);
+#pragma unroll 1
+  for (int j = lo + 2; j < lo + ng; j++) {
+    const int i = h->order[j];
+    occ.add(h->sm[i] * h->dur(i));
+  }
+  return occ.value();
+}
+
 // dispatch for non-integral SM partitions: the sequential head-blocking walk
 // with the float sm_running dust (token_backend.py:169-187); returns this
 // lane's grants
@@ -642,14 +666,7 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       if (same) {
         v = h->occv[g];   // same granted pods, all full-quantum tokens: same terms
       } else {
-        PySum occ;
-        occ.reset();
-#pragma unroll 1
-        for (int j = lo; j < lo + ng; j++) {
-          const int i = h->order[j];
-          occ.add(h->sm[i] * h->dur(i));
-        }
-        v = occ.value() / 100.0;
+        v = token_occupancy(h, lo, ng) / 100.0;
         h->occv[g] = v;
         h->occn[g] = (st & 2) ? -1 : ng;
       }

@@ -508,16 +508,8 @@ __device__ void xlh_step(HotX* h, int w, int s, XlShared* xs) {
       const int ng = h->ngr[g];
       if (ng == 0) continue;
       // dispatch order (float path) or grant-slot order (integral: order-free)
-      PySum occ;
-      occ.reset();
-      const int lo = h->seg[g];
-#pragma unroll 1
-      for (int j = lo; j < lo + ng; j++) {
-        const int i = h->order[j];
-        occ.add(h->sm[i] * h->dur(i));
-      }
       h->cov[g] += h->fullq[g] ? quantum : __longlong_as_double((long long)h->covbits[g]);
-      h->occ[g] += occ.value() / 100.0;
+      h->occ[g] += token_occupancy(h, h->seg[g], ng) / 100.0;
       continue;
     }
     if (x >= F) continue;

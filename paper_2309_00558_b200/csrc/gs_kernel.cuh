@@ -47,9 +47,14 @@ struct PySum {  // Python 3.12 builtin sum() over floats (see oracle/gs_oracle.c
   __device__ void reset() { f = 0.0; c = 0.0; n = 0; }
   __device__ void add(double x) {
     if (n++ == 0) { f = 0.0 + x; c = 0.0; return; }
-    double t = f + x;
-    if (fabs(f) >= fabs(x)) c += (f - t) + x;
-    else c += (x - t) + f;
+    // CPython adds Neumaier's term: (f - t) + x if |f| >= |x| else (x - t) + f,
+    // i.e. the exact rounding error of t = f + x (Fast2Sum with the larger
+    // operand first).  Knuth's branch-free TwoSum yields that same exact
+    // error for any finite operands, so c is bit-identical without the
+    // data-dependent branch (-fmad=false keeps every step rounded as written).
+    const double t = f + x;
+    const double bp = t - f;
+    c += (f - (t - bp)) + (x - bp);
     f = t;
   }
   __device__ double value() const {

@@ -416,11 +416,11 @@ __device__ __forceinline__ int serve_dry_run(const H* h, int i, double t_start, 
 // _serve (sim_engine.py:525-552) for pod i whose k-th new request is the
 // (base+k)-th unpinned one and which may start at most `avail` requests.
 template <class H, bool BND>
-__device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start, double t_end,
-                                             int base, int avail, int& comp, int& viol) {
+__device__ __forceinline__ int serve_replay(H* h, int i, int f, double t_start, double t_end,
+                                            int base, int avail, int& comp, int& viol) {
   const double busy = h->busy[i];
   double t = busy > t_start ? busy : t_start;
-  if (!(t < t_end - TIME_EPS)) { h->busy[i] = t; return; }
+  if (!(t < t_end - TIME_EPS)) { h->busy[i] = t; return 0; }
   int fl = h->flags[i];
   double rem = h->crem[i], arr = h->carr[i];
   const double slo = h->slo[f];
@@ -450,6 +450,7 @@ __device__ __forceinline__ void serve_replay(H* h, int i, int f, double t_start,
   h->crem[i] = rem;
   h->carr[i] = arr;
   h->flags[i] = (unsigned char)fl;
+  return taken;                                   // requests started
 }
 
 // Python sum() of sm * duration over the tokens order[lo, lo + ng) (ng >= 1).
@@ -704,7 +705,20 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
     const int i = act ? h->rank[k] : 0;
     const int f = act ? (h->fnode[i] & 0xffff) : -1 - lane;
     const double t_end = t0 + h->dur(i) * ws;
-    const int picks = act ? serve_dry_run(h, i, t0, t_end) : 0;
+    // the only granted pod of its function in a single-trip step needs no
+    // dry run: its FIFO base is 0, and the replay itself stops when the
+    // token's time runs out (after exactly the dry run's request starts) or
+    // the queue runs dry, so the requests it took are the function's "want"
+    // (measured: a gain for the classes with many pods per function, a loss
+    // for class XS, whose dry runs are short)
+    const int fnext = __shfl_down_sync(FULL, f, 1);
+    bool single = false;
+    if constexpr (H::PC > 32) {
+      const int fprev = __shfl_up_sync(FULL, f, 1);
+      single = act && ngl <= 32 && (lane == 0 || fprev != f) &&
+               (lane == 31 || k + 1 >= ngl || fnext != f);
+    }
+    const int picks = (act && !single) ? serve_dry_run(h, i, t0, t_end) : 0;
     int v = picks;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -712,14 +726,14 @@ __device__ int hot_step(H* h, int lane, int w, int s) {
       const int fo = __shfl_up_sync(FULL, f, o);
       if (lane >= o && fo == f) v += y;
     }
-    const int fnext = __shfl_down_sync(FULL, f, 1);
     const bool seg_end = act && (lane == 31 || k + 1 >= ngl || fnext != f);
     if (act) {
       const int base = h->fcarry[f] + v - picks;
       int avail = h->favail[f] - base;
-      avail = avail < 0 ? 0 : (avail > picks ? picks : avail);
+      avail = avail < 0 ? 0 : ((!single && avail > picks) ? picks : avail);
       int comp = 0, viol = 0;
-      serve_replay<H, BND>(h, i, f, t0, t_end, base, avail, comp, viol);
+      const int took = serve_replay<H, BND>(h, i, f, t0, t_end, base, avail, comp, viol);
+      if (single) v = took;
       if (comp) atomicAdd(&h->fcomp[f], comp);
       if (viol) atomicAdd(&h->fviol[f], viol);
     }

@@ -72,6 +72,7 @@ __device__ void init_run(Ctx& c) {
     s->err = 0; s->err_detail = 0; s->err_a0 = 0; s->err_a1 = 0; s->n_list = 0;
     s->grants = 0; s->decisions = 0; s->attempts = 0; s->frag = 0.0;
     s->pod_steps = 0; s->rect_scans = 0; s->min_free = c.P;
+    s->ka_arena = nullptr; s->kd_arena = nullptr; s->ki_arena = nullptr;
   }
   __syncwarp();
 }
@@ -303,9 +304,35 @@ __device__ void finish_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, in
   if (!c.sh->err) copy_out_run(*c.sc, out, host, nplaced, c.lane);
 }
 
+// While the registered set is rebuilt (initial placement, epochs, window
+// begin) the warp's shared-memory working set is idle: the sort scratch
+// (s_ka / s_kd / s_ki, Q entries each) moves there when it fits, so the
+// bitonic sorts of the rebuild hit shared memory instead of the HBM arena.
+template <class H>
+__device__ __forceinline__ void scratch_to_shared(Ctx& c, H* h) {
+  if (20u * (unsigned)c.Q > sizeof(H)) return;
+  if (c.lane == 0) {
+    char* b = reinterpret_cast<char*>(h);
+    c.sh->ka_arena = c.t->s_ka; c.sh->kd_arena = c.t->s_kd; c.sh->ki_arena = c.t->s_ki;
+    c.t->s_ka = reinterpret_cast<unsigned long long*>(b);
+    c.t->s_kd = reinterpret_cast<unsigned long long*>(b + 8 * (size_t)c.Q);
+    c.t->s_ki = reinterpret_cast<int*>(b + 16 * (size_t)c.Q);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void scratch_to_arena(Ctx& c) {
+  if (c.lane == 0 && c.sh->ka_arena) {
+    c.t->s_ka = c.sh->ka_arena; c.t->s_kd = c.sh->kd_arena; c.t->s_ki = c.sh->ki_arena;
+    c.sh->ka_arena = nullptr;
+  }
+  __syncwarp();
+}
+
 template <class H>
 __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, int run, H* h) {
   init_run(c);
+  scratch_to_shared(c, h);
   // initial pods: sorted fid order, spec order (sim_engine.py:436-441)
   if (c.lane == 0) {
     #pragma unroll 1
@@ -326,6 +353,7 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
   int peak = 0, fail_total = 0;
   if (!failed(c)) place_batch(c);
   if (!failed(c)) refresh_frag(c);
+  scratch_to_arena(c);
   bool hot_valid = false;
   long long pod_steps = 0, hot_grants = 0;   // hot-path counters kept in registers
   #pragma unroll 1
@@ -337,11 +365,13 @@ __device__ void simulate_run(Ctx& c, const gs_out_t& out, const gs_out_t& host, 
       const bool rebuild = !hot_valid || epoch || w >= c.sh->next_warm;
       if (rebuild) {
         if (hot_valid) hot_store(c, h);
+        scratch_to_shared(c, h);
         if (epoch) {
           run_epoch(c, w);
-          if (failed(c)) break;
+          if (failed(c)) { scratch_to_arena(c); break; }
         }
         window_begin(c, w);
+        scratch_to_arena(c);
         hot_valid = hot_load(c, h);
       } else {
         hot_begin_light(h, c.lane, w);

@@ -174,6 +174,10 @@ struct WarpShared {
   int n_list;
   int next_warm;          // earliest warm_at among placed, unregistered pods
   long long grants, decisions, attempts, pod_steps, rect_scans;
+  // the sort scratch's arena slices while it is redirected into the warp's
+  // idle working-set bytes (window rebuilds, gs_kernel.cu scratch_to_shared)
+  unsigned long long *ka_arena, *kd_arena;
+  int* ki_arena;
   int min_free;
   double frag;
   CtxTab tab;

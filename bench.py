@@ -299,11 +299,11 @@ def load_ncu():
         return {}
 
 
-NCU_CLASSES = os.path.join(ROOT, "profiles", "r2", "ncu_r2o.json")
+NCU_CLASSES = os.path.join(ROOT, "profiles", "r2", "ncu_r2p.json")
 
 
 def class_issue(classes):
-    """ncu evidence (profiles/r2/ncu_r2o.json) of the kernel class a config ran
+    """ncu evidence (profiles/r2/ncu_r2p.json) of the kernel class a config ran
     in: issue-slot use, IPC, SIMT efficiency, warps active, top stalls."""
     try:
         with open(NCU_CLASSES) as fh:

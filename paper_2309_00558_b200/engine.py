@@ -110,6 +110,26 @@ def _pinned_mode(batch):
     return "pool" if batch.n_fn_rows * 20 + batch.n_gpu_rows * 32 < (6 << 30) else False
 
 
+def _api_workers():
+    """Lowering processes of the pipelined API: the GPU, not the host, bounds
+    a large batch once the first block is on the device, and every forked
+    worker costs ~9 ms of page-table copying before the first block can start
+    (GS_API_WORKERS overrides)."""
+    import os
+    env = os.environ.get("GS_API_WORKERS")
+    if env:
+        return max(1, int(env))
+    return max(1, min(8, (os.cpu_count() or 1) // 2))
+
+
+def _api_parts(n):
+    import os
+    env = os.environ.get("GS_API_PARTS")
+    if env:
+        return max(1, int(env))
+    return None                   # compile_stream's default
+
+
 def _run_part(batch, device):
     from . import backend
     return backend.run_batch(batch, device=device, rows=True,
@@ -142,7 +162,8 @@ def simulate_records(scenarios, policies="fast", *, device: int = 0, errors: str
     failed: dict = {}
     jobs = []
     with ThreadPoolExecutor(max_workers=16, thread_name_prefix="gs-gpu") as pool:
-        for batch, index, errs in cc.compile_stream(scenarios, policies, caps):
+        for batch, index, errs in cc.compile_stream(scenarios, policies, caps,
+                                                    workers=_api_workers(), parts=_api_parts(len(scenarios))):
             failed.update(errs)
             if any(errors == "raise" or not isinstance(e, ValidationError)
                    for e in errs.values()):
